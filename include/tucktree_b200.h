@@ -1,0 +1,207 @@
+/*
+ * tucktree_b200 — C ABI of the B200-native stream-segment-tree engine.
+ *
+ * Drop-in boundary for the hot path of the reference library `tucktree`
+ * (arXiv 2501.06647; /root/reference/proj/core/include/tucktree/*.hpp). The
+ * reference exposes C++ only (no FFI); each entry point below names the
+ * reference function it replaces. INTEGRATION.md shows the C++ facade
+ * (namespace tucktree) and the ctypes binding built on these symbols.
+ *
+ * Conventions
+ *  - Plain pointers and sizes; no CUDA or torch types in the signatures.
+ *  - Factor matrices are column-major (layout of Eigen::MatrixXd), factor n
+ *    is D_n x r_n with leading dimension D_n; cores are row-major with the
+ *    temporal mode first (tucktree::DenseTensor).
+ *  - Status codes map 1:1 onto the reference's exception classes:
+ *      TT_EINVAL  <- std::invalid_argument  (bad shapes, ranges, theta, config)
+ *      TT_ELOGIC  <- std::logic_error       (structural impossibilities)
+ *      TT_EIO     <- std::runtime_error     (I/O)
+ *    plus TT_ECUDA / TT_ENOMEM for device failures. tt_last_error() returns the
+ *    thread-local message of the last failure.
+ *  - A failed append leaves the tree unchanged (sst.cpp:95-97).
+ *  - Threading: tt_append needs exclusive access to a tree; tt_recall,
+ *    tt_query_batch and the stat/node getters may run concurrently between
+ *    appends (sst.hpp:52-53).
+ *  - Input buffers are borrowed for the duration of the call only.
+ */
+#ifndef TUCKTREE_B200_H
+#define TUCKTREE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TT_MAX_ORDER 8
+
+typedef enum tt_status {
+  TT_OK = 0,
+  TT_EINVAL = 1,
+  TT_ELOGIC = 2,
+  TT_EIO = 3,
+  TT_ECUDA = 4,
+  TT_ENCCL = 5,
+  TT_ENOMEM = 6
+} tt_status;
+
+/* Where a caller buffer lives. */
+typedef enum tt_mem { TT_MEM_HOST = 0, TT_MEM_DEVICE = 1 } tt_mem;
+
+/* Node kinds (sst.hpp:20-24) and hit flags (query.hpp:11-14; TAIL = raw
+ * slices past the last complete leaf block). */
+enum { TT_LEAF = 0, TT_INTERMEDIATE = 1, TT_PLACEHOLDER = 2 };
+enum { TT_HIT_ENTIRE = 0, TT_HIT_PARTIAL = 1, TT_HIT_TAIL = 2 };
+
+/* Tree configuration: TreeConfig + AlsConfig (sst.hpp:38-43, tucker.hpp:17-22)
+ * plus the leaf block B (slices per leaf) and the CUDA device. */
+typedef struct tt_config {
+  int32_t order;                           /* p >= 2 (temporal + non-temporal modes) */
+  int64_t nontemporal[TT_MAX_ORDER - 1];   /* D_2..D_p                              */
+  int64_t ranks[TT_MAX_ORDER];             /* requested ranks, temporal first       */
+  double theta;                            /* pruning threshold, (0,1); default 0.7 */
+  int32_t max_iters;                       /* ALS sweeps cap; default 20            */
+  double tol;                              /* fit-change tolerance; default 0.01    */
+  uint64_t seed;                           /* ALS init seed; default 20240117       */
+  int64_t leaf_block;                      /* B >= 1 slices per leaf                */
+  int32_t device;                          /* CUDA device ordinal                   */
+  int32_t flags;                           /* TT_FLAG_*                             */
+} tt_config;
+
+/* Bookkeeping only: no decompositions, no device work (host-logic tests). */
+#define TT_FLAG_STRUCTURE_ONLY 1
+
+typedef struct tt_tree tt_tree;
+
+typedef struct tt_node_info {
+  int64_t id, begin, end; /* [begin, end) in slices */
+  int32_t kind;
+  int32_t has_decomposition;
+  int64_t left, right;
+  int64_t ranks[TT_MAX_ORDER]; /* column counts of the stored factors */
+} tt_node_info;
+
+typedef struct tt_hit {
+  int64_t node; /* 0 for a tail hit */
+  int64_t begin, end;
+  int32_t flag;
+  int32_t pad;
+} tt_hit;
+
+typedef struct tt_range {
+  int64_t ts, te;
+} tt_range;
+
+/* Output of one range query (range_query_detailed, query.hpp:48-50).
+ * Caller-provided buffers sized for the clamped requested ranks:
+ *   core:        prod_n r_n doubles (row-major, actual ranks)
+ *   factors[0]:  L x r_0  (column-major, ld = L = te - ts)
+ *   factors[m]:  D_m x r_m (column-major, ld = D_m)
+ * Outputs written by the engine: ranks (actual column counts), sweeps,
+ * converged, objective (final squared residual), nhits. */
+typedef struct tt_query_out {
+  double* core;
+  double* factors[TT_MAX_ORDER];
+  int64_t ranks[TT_MAX_ORDER];
+  int32_t sweeps;
+  int32_t converged;
+  double objective;
+  int32_t nhits;
+  int32_t pad;
+} tt_query_out;
+
+/* Host-side result of the standalone operations. */
+typedef struct tt_factors tt_factors;
+
+/* ---- errors --------------------------------------------------------------- */
+const char* tt_last_error(void);
+const char* tt_version(void);
+
+/* ---- tree (StreamSegmentTree, sst.hpp:54-105) ----------------------------- */
+/* StreamSegmentTree(TreeConfig)                            sst.hpp:56 */
+tt_status tt_tree_create(const tt_config* cfg, tt_tree** out);
+void tt_tree_destroy(tt_tree* tree);
+
+/* StreamSegmentTree::append, n slices at once (one slice = prod D doubles,
+ * row-major). Burst appends are processed level-synchronously: every new leaf
+ * block is decomposed in one batched launch, then every completed parent,
+ * level by level — result-identical to n sequential appends.  sst.hpp:64-67 */
+tt_status tt_append(tt_tree* tree, const double* slices, int64_t n, tt_mem where);
+
+/* timespan / height / stitch_count / last_append_node_touches / node_count /
+ * root / leaves                                            sst.hpp:69-91 */
+enum {
+  TT_STAT_TIMESPAN = 0,
+  TT_STAT_HEIGHT = 1,
+  TT_STAT_STITCH_COUNT = 2,
+  TT_STAT_LAST_TOUCHES = 3,
+  TT_STAT_NODE_COUNT = 4,
+  TT_STAT_ROOT = 5,
+  TT_STAT_LEAVES = 6
+};
+int64_t tt_tree_stat(const tt_tree* tree, int32_t what);
+
+/* StreamSegmentTree::node(NodeId)                          sst.hpp:90 */
+tt_status tt_node_info_get(const tt_tree* tree, int64_t id, tt_node_info* out);
+
+/* Node::decomposition download (sst.hpp:33): core (prod ranks) and factors
+ * (factors[0]: len x r0, ld = len; factors[m]: D_m x r_m).               */
+tt_status tt_node_get(const tt_tree* tree, int64_t id, double* core, double* const* factors, tt_mem where);
+
+/* Node ids created-or-re-decomposed by the most recent tt_append, in
+ * completion order (leaf, then its stitched ancestors).                   */
+tt_status tt_last_redecomposed(const tt_tree* tree, int64_t* ids, int64_t cap, int64_t* n);
+
+/* StreamSegmentTree::validate; returns the number of violations and writes
+ * them newline-separated into buf.                         sst.hpp:74-78 */
+int32_t tt_validate(const tt_tree* tree, char* buf, int64_t cap);
+
+/* ---- queries (query.hpp:33-50) -------------------------------------------- */
+/* recall(tree, ts, te, theta); theta <= 0 selects the tree's theta.        */
+tt_status tt_recall(const tt_tree* tree, int64_t ts, int64_t te, double theta, tt_hit* out, int64_t cap,
+                    int64_t* n);
+
+/* range_query_detailed over a batch: recall on the host, every query's
+ * multi-part stitch in one batched launch. `where` says where the out buffers
+ * live.                                                    query.hpp:44-50 */
+tt_status tt_query_batch(const tt_tree* tree, const tt_range* ranges, int64_t n, double theta, tt_query_out* outs,
+                         tt_mem where);
+
+/* Device time (ms, CUDA events) of the last tt_append / tt_query_batch
+ * split by phase: [0] leaf ALS, [1] stitches, [2] total device span.      */
+tt_status tt_last_timing(const tt_tree* tree, double* ms3);
+
+/* ---- standalone operations (tucker.hpp:48-49, stitch.hpp:15-36) ---------- */
+/* tucker_als(x, cfg) on device; x row-major with dims[0..p-1].            */
+tt_status tt_tucker_als(const double* x, int32_t p, const int64_t* dims, const int64_t* ranks, int32_t max_iters,
+                        double tol, uint64_t seed, int32_t device, tt_factors** out);
+
+/* stitch(parts, ranks, cfg) on device. Part i: core (row-major, part_ranks
+ * row i), factors[i*p + m] (column-major D_m x r_m; D_0 = part length).    */
+tt_status tt_stitch(int32_t nparts, int32_t p, const int64_t* part_dims, const int64_t* part_ranks,
+                    const double* const* cores, const double* const* factors, const int64_t* ranks,
+                    int32_t max_iters, double tol, uint64_t seed, int32_t device, tt_factors** out);
+
+/* partial_hit_factors(stored, begin, end) on device.       stitch.hpp:15 */
+tt_status tt_partial_hit(int32_t p, const int64_t* dims, const int64_t* ranks, const double* core,
+                         const double* const* factors, int64_t begin, int64_t end, int32_t device, tt_factors** out);
+
+int32_t tt_factors_order(const tt_factors* f);
+int64_t tt_factors_dim(const tt_factors* f, int32_t m);
+int64_t tt_factors_rank(const tt_factors* f, int32_t m);
+const double* tt_factors_core(const tt_factors* f);
+const double* tt_factors_factor(const tt_factors* f, int32_t m);
+int32_t tt_factors_sweeps(const tt_factors* f);
+int32_t tt_factors_converged(const tt_factors* f);
+const double* tt_factors_objective(const tt_factors* f); /* per-sweep squared residual (AlsTrace) */
+void tt_factors_free(tt_factors* f);
+
+/* Number of the engine's own kernels launched since process start (the bench
+ * reports the delta over its timed region).                               */
+int64_t tt_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TUCKTREE_B200_H */

@@ -1,0 +1,7 @@
+"""B200-native engine for the stream-segment-tree range-Tucker hot path
+(arXiv 2501.06647): C ABI in include/tucktree_b200.h, CUDA in csrc/, Python
+mirror of the reference API in tucktree.py."""
+from .tucktree import (  # noqa: F401
+    ENTIRE, INTERMEDIATE, LEAF, PARTIAL, PLACEHOLDER, TAIL, CudaError, HitEntry, InvalidArgument, LogicError, Node,
+    QueryResult, StreamSegmentTree, TuckerFactors, kernel_launches, lib, lib_path, stitch, tucker_als,
+)

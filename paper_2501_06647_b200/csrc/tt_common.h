@@ -1,0 +1,173 @@
+// Shared host/device definitions: problem descriptors, rank planning and
+// workspace layout. Everything here is data-independent integer arithmetic,
+// evaluated identically on the host (planning, buffer sizing) and on the
+// device (per-sweep shapes inside the ALS kernels).
+#pragma once
+
+#include <stdint.h>
+
+#ifdef __CUDACC__
+#define TT_HD __host__ __device__ __forceinline__
+#else
+#define TT_HD inline
+#endif
+
+namespace ttb {
+
+constexpr int kMaxP = 8;
+
+TT_HD int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
+TT_HD int64_t imax(int64_t a, int64_t b) { return a > b ? a : b; }
+
+TT_HD int64_t prod_except(const int64_t* a, int p, int skip) {
+  int64_t r = 1;
+  for (int m = 0; m < p; ++m)
+    if (m != skip) r *= a[m];
+  return r;
+}
+TT_HD int64_t prod_range(const int64_t* a, int b, int e) {
+  int64_t r = 1;
+  for (int m = b; m < e; ++m) r *= a[m];
+  return r;
+}
+
+// clamp_ranks (tucker.cpp:41-52): r_n <- min(r_n, D_n).
+TT_HD void clamp_ranks(int p, const int64_t* d, const int64_t* req, int64_t* rc) {
+  for (int m = 0; m < p; ++m) rc[m] = imin(req[m], d[m]);
+}
+
+// Column count returned by leading_left_singular_vectors (linalg.cpp:47):
+// k = min(rank, rows, cols) with cols = prod of the other factors' columns.
+// tucker_als requests the current column count (tucker.cpp:63-64) ...
+TT_HD int64_t leaf_mode_rank(int p, const int64_t* d, const int64_t* k, int n) {
+  return imin(imin(k[n], d[n]), prod_except(k, p, n));
+}
+// ... stitch requests the clamped rank every sweep (stitch.cpp:155-161).
+TT_HD int64_t stitch_mode_rank(int p, const int64_t* d, const int64_t* rc, const int64_t* k, int n) {
+  return imin(imin(rc[n], d[n]), prod_except(k, p, n));
+}
+
+// ---------------------------------------------------------------------------
+// Problem descriptors (device-visible PODs).
+struct LeafDesc {
+  const double* x;                 // row-major (len, D_1, ..., D_{p-1})
+  int64_t len;                     // temporal extent of this block
+  const double* init[kMaxP];       // init factors for this length (D_n x rc_n, col-major)
+  double* out_f[kMaxP];            // output factor slots (ld = D_n; factor 0: ld = len)
+  double* out_core;                // row-major core, capacity prod rc
+  double* ws;                      // workspace (leaf_ws_size doubles)
+  int32_t* status;                 // [sweeps, converged, zero, pad, k_0..k_{p-1}] (4 + kMaxP)
+  double* objective;               // max_iters doubles
+};
+
+struct StitchPart {
+  const double* core;              // row-major (rho_0, ..., rho_{p-1})
+  int64_t rho[kMaxP];
+  const double* v0;                // temporal factor of the stored node (col-major)
+  int64_t ld0;                     // its leading dimension (node length)
+  int64_t row0;                    // first row used (partial hit) or 0
+  int64_t len;                     // rows used
+  int32_t partial;                 // 1: rows [row0, row0+len) of a longer factor
+  int32_t pad;
+  const double* v[kMaxP];          // non-temporal factors, m >= 1 (D_m x rho_m)
+};
+
+struct StitchDesc {
+  int32_t part0, nparts;
+  int64_t L;                       // total temporal length
+  double* out_f[kMaxP];            // factor 0: L x rc0 (ld = L); m: D_m x rc_m
+  double* out_core;
+  double* ws;
+  int32_t* status;
+  double* objective;
+};
+
+struct Params {
+  int32_t p;
+  int32_t max_iters;
+  double tol;
+  int64_t d[kMaxP];                // d[0] ignored (per problem); d[m] = D_m
+  int64_t req[kMaxP];              // requested ranks
+  const double* stitch_init[kMaxP];  // stitch init factors U_m (m >= 1), D_m x rc_m
+};
+
+constexpr int kStatusInts = 4 + kMaxP;
+
+// ---------------------------------------------------------------------------
+// Workspace layouts (in doubles). The misc tail holds reductions, sigma, order.
+constexpr int64_t kMisc = 2048;
+
+struct LeafWs {
+  int64_t W, B1, B2, G, V, misc, total, gram_n;
+};
+
+TT_HD LeafWs leaf_ws_layout(int p, int64_t len, const int64_t* d, const int64_t* req) {
+  int64_t dd[kMaxP], rc[kMaxP];
+  dd[0] = len;
+  for (int m = 1; m < p; ++m) dd[m] = d[m];
+  clamp_ranks(p, dd, req, rc);
+  const int64_t ns = prod_range(dd, 1, p);
+  const int64_t sW = rc[0] * ns;
+  const int64_t sT = len * rc[1] * prod_range(dd, 2, p);
+  const int64_t sB = imax(sT, sW);
+  int64_t g = imin(len, prod_range(rc, 1, p));
+  for (int n = 1; n < p; ++n) g = imax(g, imin(dd[n], prod_except(rc, p, n)));
+  LeafWs w;
+  w.gram_n = g;
+  w.W = 0;
+  w.B1 = w.W + sW;
+  w.B2 = w.B1 + sB;
+  w.G = w.B2 + sB;
+  w.V = w.G + g * g;
+  w.misc = w.V + g * g;
+  w.total = w.misc + kMisc + 4 * g;
+  w.total = (w.total + 31) & ~int64_t(31);
+  return w;
+}
+
+struct StitchWs {
+  int64_t P, C, S, E, A, G, V, T1, T2, Z, WK, HH, misc, total, gram_n;
+  int64_t per_part_P, per_part_C, per_part_S, per_part_E;
+};
+
+// rcx[m] = max(rc[m], max_i rho_im): bound on every intermediate extent.
+TT_HD StitchWs stitch_ws_layout(int p, int64_t L, const int64_t* d, const int64_t* req, const int64_t* rho_max,
+                                int nparts) {
+  int64_t dd[kMaxP], rc[kMaxP], rcx[kMaxP];
+  dd[0] = L;
+  for (int m = 1; m < p; ++m) dd[m] = d[m];
+  clamp_ranks(p, dd, req, rc);
+  for (int m = 0; m < p; ++m) rcx[m] = imax(rc[m], rho_max[m]);
+  const int64_t Q = prod_range(rc, 1, p);
+  int64_t g = Q;
+  for (int n = 1; n < p; ++n) g = imax(g, imin(dd[n], prod_except(rc, p, n)));
+  int64_t pp = 0;
+  for (int m = 1; m < p; ++m) pp += rc[m] * rcx[m];
+  const int64_t chain = prod_range(rcx, 0, p);
+  int64_t z = 0;
+  for (int n = 1; n < p; ++n) z = imax(z, prod_except(rc, p, n) * dd[n]);
+  StitchWs w;
+  w.gram_n = g;
+  w.per_part_P = pp;
+  w.per_part_C = rcx[0] * Q;
+  w.per_part_S = rcx[0] * rcx[0];
+  w.per_part_E = rcx[0] * rc[0];
+  w.P = 0;
+  w.C = w.P + nparts * w.per_part_P;
+  w.S = w.C + nparts * w.per_part_C;
+  w.E = w.S + nparts * w.per_part_S;
+  w.A = w.E + nparts * w.per_part_E;
+  w.G = w.A + nparts * w.per_part_E;
+  w.V = w.G + g * g;
+  w.T1 = w.V + g * g;
+  w.T2 = w.T1 + chain;
+  w.Z = w.T2 + chain;
+  w.WK = w.Z + z;
+  w.HH = w.WK + g * rc[0];
+  w.misc = w.HH + rcx[0] * rcx[0];
+  w.total = w.misc + kMisc + 4 * g;
+  w.total = (w.total + 31) & ~int64_t(31);
+  return w;
+}
+
+}  // namespace ttb

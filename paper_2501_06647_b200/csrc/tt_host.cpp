@@ -1,0 +1,1404 @@
+// Host side of the engine: stream-segment-tree bookkeeping (sst.cpp), recall
+// (query.cpp), planning of the batched device work, device memory, and the C
+// ABI declared in include/tucktree_b200.h.
+//
+// The host owns every integer decision (node ids, ranges, kinds, hit sets,
+// touched sets, factor column counts); the device owns every floating-point
+// operation. There is no CPU numeric fallback: without a working CUDA device
+// every numeric entry point fails with TT_ECUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/tucktree_b200.h"
+#include "tt_common.h"
+
+namespace ttb {
+cudaError_t launch_leaf(const Params& prm, const LeafDesc* d_descs, int n, cudaStream_t st);
+cudaError_t launch_stitch(const Params& prm, const StitchDesc* d_descs, const StitchPart* d_parts, int n,
+                          cudaStream_t st);
+int64_t launches();
+}  // namespace ttb
+
+using namespace ttb;
+using Index = int64_t;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct TTError : std::runtime_error {
+  tt_status code;
+  TTError(tt_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void fail(tt_status c, const std::string& m) { throw TTError(c, m); }
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(TT_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+tt_status guarded(F&& f) {
+  try {
+    f();
+    return TT_OK;
+  } catch (const TTError& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_err = "out of host memory";
+    return TT_ENOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return TT_EIO;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host init factors: random_orthonormal (linalg.cpp:81-89) — libstdc++
+// mt19937_64 + a fresh normal_distribution per call, row-major draws, then a
+// Householder thin QR with the sign convention of linalg.cpp:15-31.
+std::vector<double> householder_thin_q(std::vector<double> a, Index m, Index n) {
+  const Index k = std::min(m, n);
+  std::vector<double> tau(static_cast<size_t>(k), 0.0);
+  for (Index j = 0; j < k; ++j) {
+    double* col = a.data() + j * m;
+    double xn = 0.0;
+    for (Index i = j + 1; i < m; ++i) xn += col[i] * col[i];
+    xn = std::sqrt(xn);
+    const double alpha = col[j];
+    if (xn == 0.0) {
+      tau[j] = 0.0;
+      continue;
+    }
+    const double beta = -std::copysign(std::hypot(alpha, xn), alpha);
+    tau[j] = (beta - alpha) / beta;
+    const double scale = 1.0 / (alpha - beta);
+    for (Index i = j + 1; i < m; ++i) col[i] *= scale;
+    col[j] = beta;
+    for (Index c = j + 1; c < n; ++c) {
+      double* cc = a.data() + c * m;
+      double s = cc[j];
+      for (Index i = j + 1; i < m; ++i) s += col[i] * cc[i];
+      s *= tau[j];
+      cc[j] -= s;
+      for (Index i = j + 1; i < m; ++i) cc[i] -= s * col[i];
+    }
+  }
+  std::vector<double> q(static_cast<size_t>(m * k), 0.0);
+  for (Index j = 0; j < k; ++j) q[j + j * m] = 1.0;
+  for (Index j = k - 1; j >= 0; --j) {
+    const double* v = a.data() + j * m;
+    for (Index c = j; c < k; ++c) {
+      double* qc = q.data() + c * m;
+      double s = qc[j];
+      for (Index i = j + 1; i < m; ++i) s += v[i] * qc[i];
+      s *= tau[j];
+      qc[j] -= s;
+      for (Index i = j + 1; i < m; ++i) qc[i] -= s * v[i];
+    }
+  }
+  for (Index j = 0; j < k; ++j) {
+    double* c = q.data() + j * m;
+    Index piv = 0;
+    double best = -1.0;
+    for (Index i = 0; i < m; ++i)
+      if (std::abs(c[i]) > best) {
+        best = std::abs(c[i]);
+        piv = i;
+      }
+    if (c[piv] < 0.0)
+      for (Index i = 0; i < m; ++i) c[i] = -c[i];
+  }
+  return q;
+}
+
+std::vector<double> random_orthonormal(Index rows, Index cols, std::mt19937_64& rng) {
+  if (rows < cols) fail(TT_EINVAL, "random_orthonormal: rows < cols");
+  std::normal_distribution<double> normal(0.0, 1.0);
+  std::vector<double> g(static_cast<size_t>(rows * cols));
+  for (Index i = 0; i < rows; ++i)
+    for (Index j = 0; j < cols; ++j) g[i + j * rows] = normal(rng);
+  return householder_thin_q(std::move(g), rows, cols);
+}
+
+// ---------------------------------------------------------------------------
+// Device memory.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void ensure(size_t b) {
+    if (b <= bytes) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cuda_check(cudaMalloc(&p, std::max<size_t>(b, 256)), "cudaMalloc");
+    bytes = std::max<size_t>(b, 256);
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// Bump allocator over large chunks for node decompositions (never moves).
+struct Arena {
+  std::vector<void*> chunks;
+  char* cur = nullptr;
+  size_t left = 0;
+  static constexpr size_t kChunk = size_t(256) << 20;
+  ~Arena() {
+    for (void* c : chunks) cudaFree(c);
+  }
+  double* alloc(size_t n_doubles) {
+    size_t b = (n_doubles * sizeof(double) + 255) & ~size_t(255);
+    if (b == 0) b = 256;
+    if (b > left) {
+      const size_t cb = std::max(kChunk, b);
+      void* c = nullptr;
+      cuda_check(cudaMalloc(&c, cb), "cudaMalloc(arena)");
+      chunks.push_back(c);
+      cur = static_cast<char*>(c);
+      left = cb;
+    }
+    double* r = reinterpret_cast<double*>(cur);
+    cur += b;
+    left -= b;
+    return r;
+  }
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// Per-device execution context: one stream, staging buffers and timers.
+struct Exec {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  DevBuf d_desc, d_parts, d_ws, d_status, d_obj, d_stage;
+  std::vector<char> h_status_bytes;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  explicit Exec(int dev) : device(dev) {
+    DeviceGuard g(dev);
+    cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (auto& e : ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+  }
+  ~Exec() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+  }
+  void sync() { cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize"); }
+};
+
+// Result of one batched ALS problem after readback.
+struct ProblemStatus {
+  int sweeps = 0, converged = 0, zero = 0, deficient = 0;
+  Index k[kMaxP] = {};
+  std::vector<double> objective;
+};
+
+// Uploads descriptors, runs a leaf batch, reads statuses back (synchronous).
+std::vector<ProblemStatus> run_leaf_batch(Exec& ex, const Params& prm, std::vector<LeafDesc>& descs,
+                                          const std::vector<Index>& ws_sizes) {
+  const int n = static_cast<int>(descs.size());
+  std::vector<ProblemStatus> st(static_cast<size_t>(n));
+  if (n == 0) return st;
+  size_t ws_total = 0;
+  for (Index w : ws_sizes) ws_total += static_cast<size_t>(w);
+  ex.d_ws.ensure(ws_total * sizeof(double));
+  ex.d_status.ensure(size_t(n) * kStatusInts * sizeof(int32_t));
+  ex.d_obj.ensure(size_t(n) * prm.max_iters * sizeof(double));
+  size_t off = 0;
+  for (int i = 0; i < n; ++i) {
+    descs[i].ws = ex.d_ws.as<double>() + off;
+    off += static_cast<size_t>(ws_sizes[i]);
+    descs[i].status = ex.d_status.as<int32_t>() + size_t(i) * kStatusInts;
+    descs[i].objective = ex.d_obj.as<double>() + size_t(i) * prm.max_iters;
+  }
+  ex.d_desc.ensure(sizeof(LeafDesc) * n);
+  cuda_check(cudaMemcpyAsync(ex.d_desc.p, descs.data(), sizeof(LeafDesc) * n, cudaMemcpyHostToDevice, ex.stream),
+             "upload leaf descriptors");
+  cuda_check(launch_leaf(prm, ex.d_desc.as<LeafDesc>(), n, ex.stream), "leaf_als_kernel launch");
+  std::vector<int32_t> hs(size_t(n) * kStatusInts);
+  std::vector<double> ho(size_t(n) * prm.max_iters);
+  cuda_check(cudaMemcpyAsync(hs.data(), ex.d_status.p, hs.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, ex.stream),
+             "status readback");
+  cuda_check(cudaMemcpyAsync(ho.data(), ex.d_obj.p, ho.size() * sizeof(double), cudaMemcpyDeviceToHost, ex.stream),
+             "objective readback");
+  ex.sync();
+  for (int i = 0; i < n; ++i) {
+    const int32_t* s = hs.data() + size_t(i) * kStatusInts;
+    st[i].sweeps = s[0];
+    st[i].converged = s[1];
+    st[i].zero = s[2];
+    st[i].deficient = s[3];
+    for (int m = 0; m < kMaxP; ++m) st[i].k[m] = s[4 + m];
+    st[i].objective.assign(ho.begin() + size_t(i) * prm.max_iters, ho.begin() + size_t(i) * prm.max_iters + s[0]);
+  }
+  return st;
+}
+
+std::vector<ProblemStatus> run_stitch_batch(Exec& ex, const Params& prm, std::vector<StitchDesc>& descs,
+                                            const std::vector<StitchPart>& parts, const std::vector<Index>& ws_sizes) {
+  const int n = static_cast<int>(descs.size());
+  std::vector<ProblemStatus> st(static_cast<size_t>(n));
+  if (n == 0) return st;
+  size_t ws_total = 0;
+  for (Index w : ws_sizes) ws_total += static_cast<size_t>(w);
+  ex.d_ws.ensure(ws_total * sizeof(double));
+  ex.d_status.ensure(size_t(n) * kStatusInts * sizeof(int32_t));
+  ex.d_obj.ensure(size_t(n) * prm.max_iters * sizeof(double));
+  size_t off = 0;
+  for (int i = 0; i < n; ++i) {
+    descs[i].ws = ex.d_ws.as<double>() + off;
+    off += static_cast<size_t>(ws_sizes[i]);
+    descs[i].status = ex.d_status.as<int32_t>() + size_t(i) * kStatusInts;
+    descs[i].objective = ex.d_obj.as<double>() + size_t(i) * prm.max_iters;
+  }
+  ex.d_desc.ensure(sizeof(StitchDesc) * n);
+  ex.d_parts.ensure(sizeof(StitchPart) * std::max<size_t>(parts.size(), 1));
+  cuda_check(cudaMemcpyAsync(ex.d_desc.p, descs.data(), sizeof(StitchDesc) * n, cudaMemcpyHostToDevice, ex.stream),
+             "upload stitch descriptors");
+  cuda_check(cudaMemcpyAsync(ex.d_parts.p, parts.data(), sizeof(StitchPart) * parts.size(), cudaMemcpyHostToDevice,
+                             ex.stream),
+             "upload stitch parts");
+  cuda_check(launch_stitch(prm, ex.d_desc.as<StitchDesc>(), ex.d_parts.as<StitchPart>(), n, ex.stream),
+             "stitch_als_kernel launch");
+  std::vector<int32_t> hs(size_t(n) * kStatusInts);
+  std::vector<double> ho(size_t(n) * prm.max_iters);
+  cuda_check(cudaMemcpyAsync(hs.data(), ex.d_status.p, hs.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, ex.stream),
+             "status readback");
+  cuda_check(cudaMemcpyAsync(ho.data(), ex.d_obj.p, ho.size() * sizeof(double), cudaMemcpyDeviceToHost, ex.stream),
+             "objective readback");
+  ex.sync();
+  for (int i = 0; i < n; ++i) {
+    const int32_t* s = hs.data() + size_t(i) * kStatusInts;
+    st[i].sweeps = s[0];
+    st[i].converged = s[1];
+    st[i].zero = s[2];
+    st[i].deficient = s[3];
+    for (int m = 0; m < kMaxP; ++m) st[i].k[m] = s[4 + m];
+    st[i].objective.assign(ho.begin() + size_t(i) * prm.max_iters, ho.begin() + size_t(i) * prm.max_iters + s[0]);
+  }
+  return st;
+}
+
+// Shared per-shape constants: leaf init factors per block length and the
+// stitch init factors (one rng(seed) stream per ALS call, tucker.cpp:29 and
+// stitch.cpp:135, so they are per-shape constants).
+struct InitCache {
+  int p = 0;
+  Index d[kMaxP] = {};
+  Index req[kMaxP] = {};
+  uint64_t seed = 0;
+  std::map<Index, std::vector<std::unique_ptr<DevBuf>>> leaf;  // by block length
+  std::vector<std::unique_ptr<DevBuf>> stitch;                 // m >= 1 (index m)
+
+  const std::vector<std::unique_ptr<DevBuf>>& leaf_init(Index len, cudaStream_t st) {
+    auto it = leaf.find(len);
+    if (it != leaf.end()) return it->second;
+    Index dd[kMaxP], rc[kMaxP];
+    dd[0] = len;
+    for (int m = 1; m < p; ++m) dd[m] = d[m];
+    clamp_ranks(p, dd, req, rc);
+    std::mt19937_64 rng(seed);
+    std::vector<std::unique_ptr<DevBuf>> v;
+    for (int m = 0; m < p; ++m) {
+      const auto q = random_orthonormal(dd[m], rc[m], rng);
+      auto b = std::make_unique<DevBuf>();
+      b->ensure(q.size() * sizeof(double));
+      cuda_check(cudaMemcpyAsync(b->p, q.data(), q.size() * sizeof(double), cudaMemcpyHostToDevice, st), "init upload");
+      cuda_check(cudaStreamSynchronize(st), "init upload sync");
+      v.push_back(std::move(b));
+    }
+    return leaf.emplace(len, std::move(v)).first->second;
+  }
+  void stitch_init(Params& prm, cudaStream_t st) {
+    if (stitch.empty()) {
+      std::mt19937_64 rng(seed);
+      stitch.resize(static_cast<size_t>(p));
+      for (int m = 1; m < p; ++m) {
+        const auto q = random_orthonormal(d[m], std::min(req[m], d[m]), rng);
+        stitch[m] = std::make_unique<DevBuf>();
+        stitch[m]->ensure(q.size() * sizeof(double));
+        cuda_check(cudaMemcpyAsync(stitch[m]->p, q.data(), q.size() * sizeof(double), cudaMemcpyHostToDevice, st),
+                   "stitch init upload");
+        cuda_check(cudaStreamSynchronize(st), "stitch init sync");
+      }
+    }
+    for (int m = 1; m < p; ++m) prm.stitch_init[m] = stitch[m]->as<double>();
+  }
+  // stitch.cpp:146-150 zero path: U_0 = random_orthonormal(L, r0) drawn after the U_m.
+  std::vector<double> stitch_zero_u0(Index L, Index r0) const {
+    std::mt19937_64 rng(seed);
+    for (int m = 1; m < p; ++m) (void)random_orthonormal(d[m], std::min(req[m], d[m]), rng);
+    return random_orthonormal(L, r0, rng);
+  }
+};
+
+Params make_params(int p, const Index* d, const Index* req, int max_iters, double tol) {
+  Params prm{};
+  prm.p = p;
+  prm.max_iters = max_iters;
+  prm.tol = tol;
+  for (int m = 0; m < kMaxP; ++m) {
+    prm.d[m] = m < p ? d[m] : 1;
+    prm.req[m] = m < p ? req[m] : 1;
+    prm.stitch_init[m] = nullptr;
+  }
+  return prm;
+}
+
+}  // namespace
+
+// ===========================================================================
+// Tree
+struct HostNode {
+  Index id = 0, begin = 0, end = 0;  // slices
+  int kind = TT_PLACEHOLDER;
+  Index left = 0, right = 0;
+  bool has_dec = false;
+  Index ranks[kMaxP] = {};
+  double* f[kMaxP] = {};  // device factor slots (capacity clamped ranks)
+  double* core = nullptr;
+  Index length() const { return end - begin; }
+};
+
+struct tt_tree {
+  tt_config cfg{};
+  int p = 0;
+  Index d[kMaxP] = {};  // d[0] unused
+  Index B = 1, slice = 1;
+  bool structure_only = false;
+  std::vector<HostNode> nodes;
+  Index root = 0, timespan = 0, leaves = 0, stitch_count = 0, last_touches = 0;
+  std::vector<Index> last_redec;
+  std::unique_ptr<Exec> ex;
+  std::unique_ptr<Arena> arena;
+  DevBuf tail;  // B slices (device)
+  InitCache init;
+  DevBuf stage;  // host-burst staging
+  DevBuf qout;   // query output staging (host-destination batches)
+  DevBuf tailq;  // tail-part scratch for queries
+  double timing[3] = {0, 0, 0};
+  mutable std::mutex qmu;
+
+  HostNode& node(Index id) { return nodes[static_cast<size_t>(id - 1)]; }
+  const HostNode& node(Index id) const {
+    if (id < 1 || id > static_cast<Index>(nodes.size())) fail(TT_EINVAL, "unknown node id " + std::to_string(id));
+    return nodes[static_cast<size_t>(id - 1)];
+  }
+  Index clamped(int m, Index len) const { return std::min(cfg.ranks[m], m == 0 ? len : d[m]); }
+  Index create_node(Index b_leaf, Index e_leaf) {
+    HostNode n;
+    n.id = static_cast<Index>(nodes.size() + 1);
+    n.begin = b_leaf * B;
+    n.end = e_leaf * B;
+    nodes.push_back(n);
+    return nodes.back().id;
+  }
+  void alloc_slots(HostNode& v) {
+    if (structure_only || v.core) return;
+    Index rc[kMaxP];
+    for (int m = 0; m < p; ++m) rc[m] = clamped(m, v.length());
+    v.f[0] = arena->alloc(static_cast<size_t>(v.length() * rc[0]));
+    for (int m = 1; m < p; ++m) v.f[m] = arena->alloc(static_cast<size_t>(d[m] * rc[m]));
+    v.core = arena->alloc(static_cast<size_t>(prod_range(rc, 0, p)));
+  }
+  Index height() const {
+    if (root == 0) return 0;
+    std::function<Index(Index)> depth = [&](Index id) -> Index {
+      const HostNode& v = node(id);
+      Index best = 0;
+      if (v.left) best = std::max(best, depth(v.left));
+      if (v.right) best = std::max(best, depth(v.right));
+      return best + 1;
+    };
+    return depth(root);
+  }
+};
+
+namespace {
+
+// sst.cpp:112-145 in leaf units: records the leaf and the completed parents.
+struct PendingWork {
+  std::vector<std::pair<Index, Index>> leaves;  // (node id, leaf index)
+  std::vector<Index> stitches;                  // node ids in completion order
+};
+
+void insert_leaf(tt_tree& t, Index id, Index leaf_idx, PendingWork& w) {
+  ++t.last_touches;
+  const Index b = t.node(id).begin / t.B, e = t.node(id).end / t.B;
+  if (b == leaf_idx && e == leaf_idx + 1) {
+    HostNode& v = t.node(id);
+    v.kind = TT_LEAF;
+    w.leaves.emplace_back(id, leaf_idx);
+    t.last_redec.push_back(id);
+    return;
+  }
+  const Index mid = (b + e) / 2;
+  if (leaf_idx < mid) {
+    if (t.node(id).left == 0) {
+      const Index c = t.create_node(b, mid);
+      t.node(id).left = c;
+    }
+    insert_leaf(t, t.node(id).left, leaf_idx, w);
+  } else {
+    if (t.node(id).right == 0) {
+      const Index c = t.create_node(mid, e);
+      t.node(id).right = c;
+    }
+    insert_leaf(t, t.node(id).right, leaf_idx, w);
+    if (e == leaf_idx + 1) {
+      HostNode& v = t.node(id);
+      v.kind = TT_INTERMEDIATE;
+      ++t.stitch_count;
+      w.stitches.push_back(id);
+      t.last_redec.push_back(id);
+    }
+  }
+}
+
+void add_leaf(tt_tree& t, PendingWork& w) {  // sst.cpp:94-110, in leaf units
+  t.last_touches = 0;
+  t.last_redec.clear();
+  const Index li = t.leaves;
+  if (li == 0) {
+    t.root = t.create_node(0, 1);
+  } else if (t.node(t.root).end == li * t.B) {
+    const Index promoted = t.create_node(0, 2 * li);
+    t.node(promoted).left = t.root;
+    t.root = promoted;
+  }
+  insert_leaf(t, t.root, li, w);
+  ++t.leaves;
+}
+
+void planned_final_ranks(const tt_tree& t, Index len, bool leaf, Index* out) {
+  Index dd[kMaxP], rc[kMaxP], k[kMaxP];
+  dd[0] = len;
+  for (int m = 1; m < t.p; ++m) dd[m] = t.d[m];
+  clamp_ranks(t.p, dd, t.cfg.ranks, rc);
+  for (int m = 0; m < t.p; ++m) k[m] = rc[m];
+  for (int m = 0; m < t.p; ++m)
+    k[m] = leaf ? leaf_mode_rank(t.p, dd, k, m) : stitch_mode_rank(t.p, dd, rc, k, m);
+  for (int m = 0; m < t.p; ++m) out[m] = k[m];
+}
+
+Params tree_params(tt_tree& t) {
+  Params prm = make_params(t.p, t.d, t.cfg.ranks, t.cfg.max_iters, t.cfg.tol);
+  return prm;
+}
+
+// Runs the pending leaf decompositions (block pointers given) then the stitch
+// levels, updating node ranks from the device status.
+void execute(tt_tree& t, PendingWork& w, const std::vector<const double*>& leaf_x) {
+  if (t.structure_only) {
+    for (auto& [id, li] : w.leaves) {
+      HostNode& v = t.node(id);
+      v.has_dec = true;
+      planned_final_ranks(t, v.length(), true, v.ranks);
+    }
+    for (Index id : w.stitches) {
+      HostNode& v = t.node(id);
+      v.has_dec = true;
+      planned_final_ranks(t, v.length(), false, v.ranks);
+    }
+    return;
+  }
+  Exec& ex = *t.ex;
+  DeviceGuard g(ex.device);
+  Params prm = tree_params(t);
+  cuda_check(cudaEventRecord(ex.ev[0], ex.stream), "event");
+  // ---- leaves
+  if (!w.leaves.empty()) {
+    const auto& init = t.init.leaf_init(t.B, ex.stream);
+    std::vector<LeafDesc> descs;
+    std::vector<Index> ws;
+    for (size_t i = 0; i < w.leaves.size(); ++i) {
+      HostNode& v = t.node(w.leaves[i].first);
+      t.alloc_slots(v);
+      LeafDesc dsc{};
+      dsc.x = leaf_x[i];
+      dsc.len = t.B;
+      for (int m = 0; m < t.p; ++m) {
+        dsc.init[m] = init[m]->as<double>();
+        dsc.out_f[m] = v.f[m];
+      }
+      dsc.out_core = v.core;
+      descs.push_back(dsc);
+      ws.push_back(leaf_ws_layout(t.p, t.B, t.d, t.cfg.ranks).total);
+    }
+    const auto st = run_leaf_batch(ex, prm, descs, ws);
+    for (size_t i = 0; i < w.leaves.size(); ++i) {
+      HostNode& v = t.node(w.leaves[i].first);
+      v.has_dec = true;
+      for (int m = 0; m < t.p; ++m) v.ranks[m] = st[i].k[m];
+    }
+  }
+  cuda_check(cudaEventRecord(ex.ev[1], ex.stream), "event");
+  // ---- stitches, level by level (children always complete at a lower level)
+  if (!w.stitches.empty()) {
+    t.init.stitch_init(prm, ex.stream);
+    std::map<Index, std::vector<Index>> by_level;
+    for (Index id : w.stitches) {
+      Index len = t.node(id).length() / t.B, lvl = 0;
+      while ((Index(1) << lvl) < len) ++lvl;
+      by_level[lvl].push_back(id);
+    }
+    for (auto& [lvl, ids] : by_level) {
+      std::vector<StitchDesc> descs;
+      std::vector<StitchPart> parts;
+      std::vector<Index> ws;
+      for (Index id : ids) {
+        HostNode& v = t.node(id);
+        t.alloc_slots(v);
+        StitchDesc dsc{};
+        dsc.part0 = static_cast<int32_t>(parts.size());
+        dsc.nparts = 2;
+        dsc.L = v.length();
+        Index rho_max[kMaxP] = {};
+        for (Index cid : {v.left, v.right}) {
+          const HostNode& c = t.node(cid);
+          if (!c.has_dec) fail(TT_ELOGIC, "stitch child has no decomposition");
+          StitchPart sp{};
+          sp.core = c.core;
+          for (int m = 0; m < t.p; ++m) {
+            sp.rho[m] = c.ranks[m];
+            rho_max[m] = std::max(rho_max[m], c.ranks[m]);
+            sp.v[m] = c.f[m];
+          }
+          sp.v0 = c.f[0];
+          sp.ld0 = c.length();
+          sp.row0 = 0;
+          sp.len = c.length();
+          sp.partial = 0;
+          parts.push_back(sp);
+        }
+        for (int m = 0; m < t.p; ++m) dsc.out_f[m] = v.f[m];
+        dsc.out_core = v.core;
+        descs.push_back(dsc);
+        ws.push_back(stitch_ws_layout(t.p, v.length(), t.d, t.cfg.ranks, rho_max, 2).total);
+      }
+      const auto st = run_stitch_batch(ex, prm, descs, parts, ws);
+      for (size_t i = 0; i < ids.size(); ++i) {
+        HostNode& v = t.node(ids[i]);
+        v.has_dec = true;
+        for (int m = 0; m < t.p; ++m) v.ranks[m] = st[i].k[m];
+        if (st[i].zero) {
+          const Index r0 = t.clamped(0, v.length());
+          const auto u0 = t.init.stitch_zero_u0(v.length(), r0);
+          cuda_check(cudaMemcpyAsync(v.f[0], u0.data(), u0.size() * sizeof(double), cudaMemcpyHostToDevice, ex.stream),
+                     "zero-path upload");
+          ex.sync();
+        }
+      }
+    }
+  }
+  cuda_check(cudaEventRecord(ex.ev[2], ex.stream), "event");
+  ex.sync();
+  float a = 0, b = 0;
+  cudaEventElapsedTime(&a, ex.ev[0], ex.ev[1]);
+  cudaEventElapsedTime(&b, ex.ev[1], ex.ev[2]);
+  t.timing[0] = a;
+  t.timing[1] = b;
+  t.timing[2] = a + b;
+}
+
+// query.cpp:9-31 plus the leaf-block rule (an overlapping leaf is always a hit).
+void collect_hits(const tt_tree& t, Index id, Index ts, Index te, double theta, std::vector<tt_hit>& out) {
+  const HostNode& v = t.node(id);
+  const Index overlap = std::min(te, v.end) - std::max(ts, v.begin);
+  if (v.kind != TT_PLACEHOLDER &&
+      (static_cast<double>(overlap) >= theta * static_cast<double>(v.length()) || v.kind == TT_LEAF)) {
+    const bool contained = v.begin >= ts && v.end <= te;
+    out.push_back(tt_hit{id, std::max(ts, v.begin), std::min(te, v.end), contained ? TT_HIT_ENTIRE : TT_HIT_PARTIAL, 0});
+    return;
+  }
+  if (v.left && te <= t.node(v.left).end) {
+    collect_hits(t, v.left, ts, te, theta, out);
+  } else if (v.right && ts >= t.node(v.right).begin) {
+    collect_hits(t, v.right, ts, te, theta, out);
+  } else {
+    if (!v.left || !v.right) fail(TT_ELOGIC, "recall: query spans an unmaterialized range");
+    collect_hits(t, v.left, ts, te, theta, out);
+    collect_hits(t, v.right, ts, te, theta, out);
+  }
+}
+
+std::vector<tt_hit> recall(const tt_tree& t, Index ts, Index te, double theta_in) {  // query.cpp:35-47
+  if (ts < 0 || ts >= te || te > t.timespan) fail(TT_EINVAL, "recall: query range must satisfy 0 <= ts < te <= T");
+  const double theta = theta_in > 0.0 ? theta_in : t.cfg.theta;
+  if (!(theta > 0.0 && theta < 1.0)) fail(TT_EINVAL, "recall: theta must be in (0, 1)");
+  std::vector<tt_hit> out;
+  const Index tb = t.leaves * t.B;
+  if (ts < tb) collect_hits(t, t.root, ts, std::min(te, tb), theta, out);
+  if (te > tb) out.push_back(tt_hit{0, std::max(ts, tb), te, TT_HIT_TAIL, 0});
+  return out;
+}
+
+}  // namespace
+
+// ===========================================================================
+// Standalone factors handle
+struct tt_factors {
+  int p = 0;
+  Index dims[kMaxP] = {}, ranks[kMaxP] = {};
+  std::vector<double> core;
+  std::vector<std::vector<double>> f;
+  std::vector<double> objective;
+  int sweeps = 0, converged = 0;
+};
+
+extern "C" {
+
+const char* tt_last_error(void) { return g_err.c_str(); }
+const char* tt_version(void) { return "tucktree_b200 0.1 (sm_100a)"; }
+int64_t tt_kernel_launches(void) { return launches(); }
+
+tt_status tt_tree_create(const tt_config* cfg, tt_tree** out) {
+  return guarded([&] {
+    if (!cfg || !out) fail(TT_EINVAL, "tt_tree_create: null argument");
+    *out = nullptr;
+    const int p = cfg->order;
+    if (p < 2 || p > TT_MAX_ORDER) fail(TT_EINVAL, "StreamSegmentTree: order must be in [2, 8]");
+    for (int m = 0; m < p - 1; ++m)
+      if (cfg->nontemporal[m] < 1) fail(TT_EINVAL, "StreamSegmentTree: extents must be >= 1");
+    for (int m = 0; m < p; ++m)
+      if (cfg->ranks[m] < 1) fail(TT_EINVAL, "StreamSegmentTree: ranks must be >= 1");
+    if (!(cfg->theta > 0.0 && cfg->theta < 1.0)) fail(TT_EINVAL, "StreamSegmentTree: theta must be in (0, 1)");
+    if (cfg->max_iters < 1) fail(TT_EINVAL, "max_iters must be >= 1");
+    if (cfg->tol <= 0.0) fail(TT_EINVAL, "tol must be > 0");
+    if (cfg->leaf_block < 1) fail(TT_EINVAL, "leaf_block must be >= 1");
+    auto t = std::make_unique<tt_tree>();
+    t->cfg = *cfg;
+    t->p = p;
+    t->B = cfg->leaf_block;
+    t->d[0] = 1;
+    t->slice = 1;
+    for (int m = 1; m < p; ++m) {
+      t->d[m] = cfg->nontemporal[m - 1];
+      t->slice *= t->d[m];
+    }
+    t->structure_only = (cfg->flags & TT_FLAG_STRUCTURE_ONLY) != 0;
+    t->init.p = p;
+    for (int m = 0; m < p; ++m) {
+      t->init.d[m] = t->d[m];
+      t->init.req[m] = cfg->ranks[m];
+    }
+    t->init.seed = cfg->seed;
+    if (!t->structure_only) {
+      int ndev = 0;
+      if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        fail(TT_ECUDA, "no CUDA device: the engine has no CPU fallback");
+      if (cfg->device < 0 || cfg->device >= ndev) fail(TT_EINVAL, "device ordinal out of range");
+      t->ex = std::make_unique<Exec>(cfg->device);
+      DeviceGuard g(cfg->device);
+      t->arena = std::make_unique<Arena>();
+      t->tail.ensure(static_cast<size_t>(t->B * t->slice) * sizeof(double));
+    }
+    *out = t.release();
+  });
+}
+
+void tt_tree_destroy(tt_tree* tree) {
+  if (!tree) return;
+  if (tree->ex) {
+    DeviceGuard g(tree->ex->device);
+    delete tree;
+  } else {
+    delete tree;
+  }
+}
+
+tt_status tt_append(tt_tree* t, const double* slices, int64_t n, tt_mem where) {
+  return guarded([&] {
+    if (!t) fail(TT_EINVAL, "append: null tree");
+    if (n < 0) fail(TT_EINVAL, "append: negative slice count");
+    if (n == 0) return;
+    if (!slices && !t->structure_only) fail(TT_EINVAL, "append: null slices");
+    const Index ss = t->slice, B = t->B;
+    const Index tail0 = t->timespan - t->leaves * B;
+    const Index nblocks = (tail0 + n) / B;
+    std::vector<const double*> leaf_x;
+    const double* src = slices;  // device view of the new slices
+    std::unique_ptr<DeviceGuard> g;
+    if (!t->structure_only) {
+      g = std::make_unique<DeviceGuard>(t->ex->device);
+      if (where == TT_MEM_HOST) {
+        t->stage.ensure(static_cast<size_t>(n * ss) * sizeof(double));
+        cuda_check(cudaMemcpyAsync(t->stage.p, slices, static_cast<size_t>(n * ss) * sizeof(double),
+                                   cudaMemcpyHostToDevice, t->ex->stream),
+                   "append upload");
+        src = t->stage.as<double>();
+      }
+      // Block 0 completes the buffered tail; later blocks read straight from src.
+      Index consumed = 0;
+      for (Index j = 0; j < nblocks; ++j) {
+        if (j == 0 && tail0 > 0) {
+          const Index need = B - tail0;
+          cuda_check(cudaMemcpyAsync(t->tail.as<double>() + tail0 * ss, src, static_cast<size_t>(need * ss) * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, t->ex->stream),
+                     "tail fill");
+          leaf_x.push_back(t->tail.as<double>());
+          consumed = need;
+        } else {
+          leaf_x.push_back(src + consumed * ss);
+          consumed += B;
+        }
+      }
+      (void)consumed;
+    }
+    // Bookkeeping, one slice at a time (reference append semantics).
+    PendingWork w;
+    std::vector<Index> all_redec;
+    for (Index i = 0; i < n; ++i) {
+      ++t->timespan;
+      if (t->timespan - t->leaves * B == B) {
+        add_leaf(*t, w);
+        all_redec.insert(all_redec.end(), t->last_redec.begin(), t->last_redec.end());
+      } else {
+        t->last_touches = 0;
+        t->last_redec.clear();
+      }
+    }
+    execute(*t, w, leaf_x);
+    if (!t->structure_only) {
+      // New tail = slices past the last full block (after the leaf kernels read the old tail).
+      const Index tail1 = t->timespan - t->leaves * B;
+      if (tail1 > 0) {
+        const Index first_new = n - tail1;  // index into the new slices
+        if (first_new >= 0) {
+          cuda_check(cudaMemcpyAsync(t->tail.p, src + first_new * ss, static_cast<size_t>(tail1 * ss) * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, t->ex->stream),
+                     "tail store");
+        } else {  // no block completed: old tail + all new slices
+          cuda_check(cudaMemcpyAsync(t->tail.as<double>() + tail0 * ss, src, static_cast<size_t>(n * ss) * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, t->ex->stream),
+                     "tail append");
+        }
+      }
+      t->ex->sync();
+    }
+    t->last_redec = all_redec;
+  });
+}
+
+int64_t tt_tree_stat(const tt_tree* t, int32_t what) {
+  if (!t) return -1;
+  switch (what) {
+    case TT_STAT_TIMESPAN: return t->timespan;
+    case TT_STAT_HEIGHT: return t->height();
+    case TT_STAT_STITCH_COUNT: return t->stitch_count;
+    case TT_STAT_LAST_TOUCHES: return t->last_touches;
+    case TT_STAT_NODE_COUNT: return static_cast<int64_t>(t->nodes.size());
+    case TT_STAT_ROOT: return t->root;
+    case TT_STAT_LEAVES: return t->leaves;
+    default: return -1;
+  }
+}
+
+tt_status tt_node_info_get(const tt_tree* t, int64_t id, tt_node_info* out) {
+  return guarded([&] {
+    if (!t || !out) fail(TT_EINVAL, "null argument");
+    const HostNode& v = t->node(id);
+    std::memset(out, 0, sizeof(*out));
+    out->id = v.id;
+    out->begin = v.begin;
+    out->end = v.end;
+    out->kind = v.kind;
+    out->has_decomposition = v.has_dec;
+    out->left = v.left;
+    out->right = v.right;
+    for (int m = 0; m < t->p; ++m) out->ranks[m] = v.ranks[m];
+  });
+}
+
+tt_status tt_node_get(const tt_tree* t, int64_t id, double* core, double* const* factors, tt_mem where) {
+  return guarded([&] {
+    if (!t) fail(TT_EINVAL, "null tree");
+    const HostNode& v = t->node(id);
+    if (!v.has_dec || t->structure_only) fail(TT_ELOGIC, "node has no decomposition");
+    DeviceGuard g(t->ex->device);
+    const cudaMemcpyKind kind = where == TT_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    if (core)
+      cuda_check(cudaMemcpyAsync(core, v.core, static_cast<size_t>(prod_range(v.ranks, 0, t->p)) * sizeof(double), kind,
+                                 t->ex->stream),
+                 "node core download");
+    for (int m = 0; m < t->p; ++m) {
+      if (!factors || !factors[m]) continue;
+      const Index rows = m == 0 ? v.length() : t->d[m];
+      cuda_check(cudaMemcpyAsync(factors[m], v.f[m], static_cast<size_t>(rows * v.ranks[m]) * sizeof(double), kind,
+                                 t->ex->stream),
+                 "node factor download");
+    }
+    t->ex->sync();
+  });
+}
+
+tt_status tt_last_redecomposed(const tt_tree* t, int64_t* ids, int64_t cap, int64_t* n) {
+  return guarded([&] {
+    if (!t || !n) fail(TT_EINVAL, "null argument");
+    *n = static_cast<int64_t>(t->last_redec.size());
+    for (size_t i = 0; i < t->last_redec.size() && static_cast<int64_t>(i) < cap; ++i) ids[i] = t->last_redec[i];
+  });
+}
+
+tt_status tt_last_timing(const tt_tree* t, double* ms3) {
+  return guarded([&] {
+    if (!t || !ms3) fail(TT_EINVAL, "null argument");
+    for (int i = 0; i < 3; ++i) ms3[i] = t->timing[i];
+  });
+}
+
+// sst.cpp:159-295 (structural invariants; leaf length B).
+int32_t tt_validate(const tt_tree* t, char* buf, int64_t cap) {
+  if (!t) return -1;
+  std::vector<std::string> out;
+  auto flag = [&out](std::string s) { out.push_back(std::move(s)); };
+  auto label = [](const HostNode& n) {
+    return "node " + std::to_string(n.id) + " [" + std::to_string(n.begin) + "," + std::to_string(n.end) + ")";
+  };
+  const Index B = t->B, T = t->leaves * B;
+  auto ceil_log2 = [](Index n) {
+    Index l = 0, q = 1;
+    while (q < n) {
+      q *= 2;
+      ++l;
+    }
+    return l;
+  };
+  if (t->leaves == 0) {
+    if (t->root) flag("empty tree has a root");
+  } else if (!t->root) {
+    flag("non-empty tree has no root");
+  } else {
+    const Index N = static_cast<Index>(t->nodes.size());
+    auto valid = [N](Index id) { return id >= 1 && id <= N; };
+    for (const HostNode& v : t->nodes) {
+      if (v.begin < 0 || v.begin >= v.end) flag(label(v) + ": malformed range");
+      if ((v.left && !valid(v.left)) || (v.right && !valid(v.right))) {
+        flag(label(v) + ": child id unknown");
+        continue;
+      }
+      if (v.kind == TT_LEAF) {
+        if (v.length() != B) flag(label(v) + ": leaf range must have length 1");
+        if (v.left || v.right) flag(label(v) + ": leaf must not have children");
+        if (!v.has_dec) flag(label(v) + ": leaf is missing its decomposition");
+      } else if (v.kind == TT_INTERMEDIATE) {
+        if (!v.left || !v.right) {
+          flag(label(v) + ": intermediate must have two children");
+        } else {
+          const HostNode& l = t->node(v.left);
+          const HostNode& r = t->node(v.right);
+          if (l.begin != v.begin || l.end != r.begin || r.end != v.end) flag(label(v) + ": children ranges are not adjoint");
+          if (l.kind == TT_PLACEHOLDER || r.kind == TT_PLACEHOLDER) flag(label(v) + ": intermediate has a placeholder child");
+          if (!v.has_dec) flag(label(v) + ": intermediate is missing its decomposition");
+        }
+      } else {
+        if (v.has_dec) flag(label(v) + ": placeholder carries a decomposition");
+        if (!(v.begin < T && T <= v.end)) flag(label(v) + ": placeholder does not straddle the write frontier");
+        if (!v.left && v.right) flag(label(v) + ": placeholder has a right child without a left child");
+        if (!v.left && !v.right) flag(label(v) + ": placeholder has no children");
+      }
+      if (v.kind != TT_PLACEHOLDER && v.end > T) flag(label(v) + ": materialized node extends past the timespan");
+    }
+    std::vector<const HostNode*> lv;
+    for (const HostNode& v : t->nodes)
+      if (v.kind == TT_LEAF) lv.push_back(&v);
+    std::sort(lv.begin(), lv.end(), [](const HostNode* a, const HostNode* b) { return a->begin < b->begin; });
+    Index expected = 0;
+    for (const HostNode* l : lv) {
+      if (l->begin != expected) {
+        flag(label(*l) + ": leaf tiling gap or overlap");
+        break;
+      }
+      expected = l->end;
+    }
+    if (expected != T && out.empty()) flag("leaves do not cover the timespan");
+    const HostNode& r = t->node(t->root);
+    const Index span = (t->leaves == 1 ? 1 : (Index(1) << ceil_log2(t->leaves))) * B;
+    if (r.begin != 0 || r.end != span) flag(label(r) + ": root range wrong");
+    if (t->height() != ceil_log2(t->leaves) + 1) flag("height violates the height law");
+  }
+  std::string all;
+  for (auto& s : out) all += s + "\n";
+  if (buf && cap > 0) {
+    std::strncpy(buf, all.c_str(), static_cast<size_t>(cap - 1));
+    buf[cap - 1] = '\0';
+  }
+  return static_cast<int32_t>(out.size());
+}
+
+tt_status tt_recall(const tt_tree* t, int64_t ts, int64_t te, double theta, tt_hit* out, int64_t cap, int64_t* n) {
+  return guarded([&] {
+    if (!t || !n) fail(TT_EINVAL, "null argument");
+    const auto hits = recall(*t, ts, te, theta);
+    *n = static_cast<int64_t>(hits.size());
+    for (size_t i = 0; i < hits.size() && static_cast<int64_t>(i) < cap; ++i) out[i] = hits[i];
+  });
+}
+
+tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, double theta, tt_query_out* outs,
+                         tt_mem where) {
+  return guarded([&] {
+    if (!tc) fail(TT_EINVAL, "null tree");
+    tt_tree* t = const_cast<tt_tree*>(tc);
+    if (n <= 0) return;
+    if (!ranges || !outs) fail(TT_EINVAL, "null ranges/outs");
+    if (t->structure_only) fail(TT_ELOGIC, "range_query on a structure-only tree");
+    std::lock_guard<std::mutex> lk(t->qmu);
+    const int p = t->p;
+    // recall for every query first: an invalid range fails the batch before any device work
+    std::vector<std::vector<tt_hit>> hits(static_cast<size_t>(n));
+    for (int64_t q = 0; q < n; ++q) hits[q] = recall(*t, ranges[q].ts, ranges[q].te, theta);
+    Exec& ex = *t->ex;
+    DeviceGuard g(ex.device);
+    Params prm = tree_params(*t);
+    t->init.stitch_init(prm, ex.stream);
+    cuda_check(cudaEventRecord(ex.ev[0], ex.stream), "event");
+    // ---- tail parts: tucker_als of the raw tail sub-range
+    struct TailSlot {
+      double* f[kMaxP];
+      double* core;
+      Index len;
+      Index ranks[kMaxP];
+    };
+    std::vector<TailSlot> tails(static_cast<size_t>(n));
+    {
+      std::vector<LeafDesc> descs;
+      std::vector<Index> ws, which;
+      size_t need = 0;
+      const Index tb = t->leaves * t->B;
+      std::vector<std::pair<int64_t, Index>> tl;  // (query, len)
+      for (int64_t q = 0; q < n; ++q)
+        for (const tt_hit& h : hits[q])
+          if (h.flag == TT_HIT_TAIL) tl.emplace_back(q, h.end - h.begin);
+      for (auto& [q, len] : tl) {
+        Index rc[kMaxP];
+        for (int m = 0; m < p; ++m) rc[m] = t->clamped(m, len);
+        need += static_cast<size_t>(len * rc[0] + prod_range(rc, 0, p));
+        for (int m = 1; m < p; ++m) need += static_cast<size_t>(t->d[m] * rc[m]);
+        need += 64 * static_cast<size_t>(p);
+      }
+      if (!tl.empty()) {
+        t->tailq.ensure(need * sizeof(double));
+        double* cur = t->tailq.as<double>();
+        auto take = [&cur](Index nd) {
+          double* r = cur;
+          cur += (nd + 31) & ~Index(31);
+          return r;
+        };
+        for (auto& [q, len] : tl) {
+          TailSlot& s = tails[q];
+          s.len = len;
+          Index rc[kMaxP];
+          for (int m = 0; m < p; ++m) rc[m] = t->clamped(m, len);
+          s.f[0] = take(len * rc[0]);
+          for (int m = 1; m < p; ++m) s.f[m] = take(t->d[m] * rc[m]);
+          s.core = take(prod_range(rc, 0, p));
+          const tt_hit& h = hits[q].back();
+          const auto& init = t->init.leaf_init(len, ex.stream);
+          LeafDesc dsc{};
+          dsc.x = t->tail.as<double>() + (h.begin - tb) * t->slice;
+          dsc.len = len;
+          for (int m = 0; m < p; ++m) {
+            dsc.init[m] = init[m]->as<double>();
+            dsc.out_f[m] = s.f[m];
+          }
+          dsc.out_core = s.core;
+          descs.push_back(dsc);
+          ws.push_back(leaf_ws_layout(p, len, t->d, t->cfg.ranks).total);
+          which.push_back(q);
+        }
+        const auto st = run_leaf_batch(ex, prm, descs, ws);
+        for (size_t i = 0; i < which.size(); ++i)
+          for (int m = 0; m < p; ++m) tails[which[i]].ranks[m] = st[i].k[m];
+      }
+    }
+    cuda_check(cudaEventRecord(ex.ev[1], ex.stream), "event");
+    // ---- stitches, chunked by workspace budget
+    const size_t kBudget = size_t(3) << 30;  // bytes of workspace + staging per chunk
+    int64_t q0 = 0;
+    while (q0 < n) {
+      std::vector<StitchDesc> descs;
+      std::vector<StitchPart> parts;
+      std::vector<Index> ws;
+      std::vector<size_t> out_off;
+      size_t used = 0, out_need = 0;
+      int64_t q1 = q0;
+      for (; q1 < n; ++q1) {
+        const Index L = ranges[q1].te - ranges[q1].ts;
+        Index rho_max[kMaxP] = {};
+        std::vector<StitchPart> qp;
+        for (const tt_hit& h : hits[q1]) {
+          StitchPart sp{};
+          if (h.flag == TT_HIT_TAIL) {
+            const TailSlot& s = tails[q1];
+            sp.core = s.core;
+            for (int m = 0; m < p; ++m) {
+              sp.rho[m] = s.ranks[m];
+              sp.v[m] = s.f[m];
+            }
+            sp.v0 = s.f[0];
+            sp.ld0 = s.len;
+            sp.row0 = 0;
+            sp.len = s.len;
+            sp.partial = 0;
+          } else {
+            const HostNode& v = t->node(h.node);
+            if (!v.has_dec) fail(TT_ELOGIC, "range_query: hit node has no decomposition");
+            sp.core = v.core;
+            for (int m = 0; m < p; ++m) {
+              sp.rho[m] = v.ranks[m];
+              sp.v[m] = v.f[m];
+            }
+            sp.v0 = v.f[0];
+            sp.ld0 = v.length();
+            sp.row0 = h.begin - v.begin;
+            sp.len = h.end - h.begin;
+            sp.partial = h.flag == TT_HIT_PARTIAL ? 1 : 0;
+          }
+          for (int m = 0; m < p; ++m) rho_max[m] = std::max(rho_max[m], sp.rho[m]);
+          qp.push_back(sp);
+        }
+        const Index wsz = stitch_ws_layout(p, L, t->d, t->cfg.ranks, rho_max, static_cast<int>(qp.size())).total;
+        Index rc[kMaxP];
+        for (int m = 0; m < p; ++m) rc[m] = t->clamped(m, L);
+        size_t onum = 0;
+        if (where == TT_MEM_HOST) {
+          onum = static_cast<size_t>(L * rc[0] + prod_range(rc, 0, p));
+          for (int m = 1; m < p; ++m) onum += static_cast<size_t>(t->d[m] * rc[m]);
+          onum += 32 * static_cast<size_t>(p + 1);
+        }
+        const size_t add = (static_cast<size_t>(wsz) + onum) * sizeof(double);
+        if (q1 > q0 && used + add > kBudget) break;
+        used += add;
+        StitchDesc dsc{};
+        dsc.part0 = static_cast<int32_t>(parts.size());
+        dsc.nparts = static_cast<int32_t>(qp.size());
+        dsc.L = L;
+        parts.insert(parts.end(), qp.begin(), qp.end());
+        descs.push_back(dsc);
+        ws.push_back(wsz);
+        out_off.push_back(out_need);
+        out_need += onum;
+      }
+      // output buffers
+      if (where == TT_MEM_HOST) t->qout.ensure(out_need * sizeof(double));
+      for (int64_t q = q0; q < q1; ++q) {
+        StitchDesc& dsc = descs[q - q0];
+        const Index L = dsc.L;
+        Index rc[kMaxP];
+        for (int m = 0; m < p; ++m) rc[m] = t->clamped(m, L);
+        if (where == TT_MEM_DEVICE) {
+          for (int m = 0; m < p; ++m) dsc.out_f[m] = outs[q].factors[m];
+          dsc.out_core = outs[q].core;
+        } else {
+          double* cur = t->qout.as<double>() + out_off[q - q0];
+          auto take = [&cur](Index nd) {
+            double* r = cur;
+            cur += (nd + 31) & ~Index(31);
+            return r;
+          };
+          dsc.out_f[0] = take(L * rc[0]);
+          for (int m = 1; m < p; ++m) dsc.out_f[m] = take(t->d[m] * rc[m]);
+          dsc.out_core = take(prod_range(rc, 0, p));
+        }
+      }
+      const auto st = run_stitch_batch(ex, prm, descs, parts, ws);
+      for (int64_t q = q0; q < q1; ++q) {
+        const ProblemStatus& s = st[q - q0];
+        tt_query_out& o = outs[q];
+        const Index L = descs[q - q0].L;
+        Index k[kMaxP];
+        for (int m = 0; m < p; ++m) k[m] = s.k[m];
+        if (s.zero) {
+          for (int m = 0; m < p; ++m) k[m] = t->clamped(m, L);
+          const auto u0 = t->init.stitch_zero_u0(L, k[0]);
+          cuda_check(cudaMemcpyAsync(descs[q - q0].out_f[0], u0.data(), u0.size() * sizeof(double),
+                                     cudaMemcpyHostToDevice, ex.stream),
+                     "zero-path upload");
+          ex.sync();
+        }
+        for (int m = 0; m < TT_MAX_ORDER; ++m) o.ranks[m] = m < p ? k[m] : 0;
+        o.sweeps = s.sweeps;
+        o.converged = s.converged;
+        o.objective = s.objective.empty() ? 0.0 : s.objective.back();
+        o.nhits = static_cast<int32_t>(hits[q].size());
+        if (where == TT_MEM_HOST) {
+          const StitchDesc& dsc = descs[q - q0];
+          if (o.core)
+            cuda_check(cudaMemcpyAsync(o.core, dsc.out_core, static_cast<size_t>(prod_range(k, 0, p)) * sizeof(double),
+                                       cudaMemcpyDeviceToHost, ex.stream),
+                       "query core download");
+          for (int m = 0; m < p; ++m) {
+            if (!o.factors[m]) continue;
+            const Index rows = m == 0 ? L : t->d[m];
+            cuda_check(cudaMemcpyAsync(o.factors[m], dsc.out_f[m], static_cast<size_t>(rows * k[m]) * sizeof(double),
+                                       cudaMemcpyDeviceToHost, ex.stream),
+                       "query factor download");
+          }
+        }
+      }
+      ex.sync();
+      q0 = q1;
+    }
+    cuda_check(cudaEventRecord(ex.ev[2], ex.stream), "event");
+    ex.sync();
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, ex.ev[0], ex.ev[1]);
+    cudaEventElapsedTime(&b, ex.ev[1], ex.ev[2]);
+    t->timing[0] = a;
+    t->timing[1] = b;
+    t->timing[2] = a + b;
+  });
+}
+
+// ---------------------------------------------------------------------------
+// Standalone operations.
+namespace {
+struct StandaloneCtx {
+  std::unique_ptr<Exec> ex;
+  int device = -1;
+};
+StandaloneCtx& standalone(int device) {
+  static std::mutex mu;
+  static std::map<int, std::unique_ptr<StandaloneCtx>> ctx;
+  std::lock_guard<std::mutex> lk(mu);
+  auto& c = ctx[device];
+  if (!c) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      fail(TT_ECUDA, "no CUDA device: the engine has no CPU fallback");
+    if (device < 0 || device >= ndev) fail(TT_EINVAL, "device ordinal out of range");
+    c = std::make_unique<StandaloneCtx>();
+    c->ex = std::make_unique<Exec>(device);
+    c->device = device;
+  }
+  return *c;
+}
+
+std::vector<double> download(const double* d, size_t n, cudaStream_t st) {
+  std::vector<double> h(n);
+  if (n) cuda_check(cudaMemcpyAsync(h.data(), d, n * sizeof(double), cudaMemcpyDeviceToHost, st), "download");
+  return h;
+}
+double* upload(DevBuf& b, const double* h, size_t n, cudaStream_t st) {
+  b.ensure(std::max<size_t>(n, 1) * sizeof(double));
+  if (n) cuda_check(cudaMemcpyAsync(b.p, h, n * sizeof(double), cudaMemcpyHostToDevice, st), "upload");
+  return b.as<double>();
+}
+}  // namespace
+
+tt_status tt_tucker_als(const double* x, int32_t p, const int64_t* dims, const int64_t* ranks, int32_t max_iters,
+                        double tol, uint64_t seed, int32_t device, tt_factors** out) {
+  return guarded([&] {
+    if (!x || !dims || !ranks || !out) fail(TT_EINVAL, "null argument");
+    *out = nullptr;
+    if (p < 2 || p > TT_MAX_ORDER) fail(TT_EINVAL, "tucker_als: order must be in [2, 8]");
+    if (max_iters < 1) fail(TT_EINVAL, "tucker_als: max_iters must be >= 1");
+    if (tol <= 0.0) fail(TT_EINVAL, "tucker_als: tol must be > 0");
+    for (int m = 0; m < p; ++m) {
+      if (dims[m] < 1) fail(TT_EINVAL, "Shape: all dims must be >= 1");
+      if (ranks[m] < 1) fail(TT_EINVAL, "clamp_ranks: ranks must be >= 1");
+    }
+    StandaloneCtx& c = standalone(device);
+    Exec& ex = *c.ex;
+    DeviceGuard g(device);
+    Index d[kMaxP], rq[kMaxP], rc[kMaxP];
+    for (int m = 0; m < kMaxP; ++m) {
+      d[m] = m < p ? dims[m] : 1;
+      rq[m] = m < p ? ranks[m] : 1;
+    }
+    clamp_ranks(p, d, rq, rc);
+    InitCache init;
+    init.p = p;
+    for (int m = 0; m < p; ++m) {
+      init.d[m] = d[m];
+      init.req[m] = rq[m];
+    }
+    init.seed = seed;
+    const auto& iv = init.leaf_init(d[0], ex.stream);
+    DevBuf bx, bout;
+    const size_t nx = static_cast<size_t>(prod_range(d, 0, p));
+    const double* dx = upload(bx, x, nx, ex.stream);
+    size_t need = static_cast<size_t>(prod_range(rc, 0, p));
+    for (int m = 0; m < p; ++m) need += static_cast<size_t>(d[m] * rc[m]) + 32;
+    bout.ensure(need * sizeof(double));
+    LeafDesc dsc{};
+    dsc.x = dx;
+    dsc.len = d[0];
+    double* cur = bout.as<double>();
+    for (int m = 0; m < p; ++m) {
+      dsc.init[m] = iv[m]->as<double>();
+      dsc.out_f[m] = cur;
+      cur += d[m] * rc[m] + 16;
+    }
+    dsc.out_core = cur;
+    Params prm = make_params(p, d, rq, max_iters, tol);
+    std::vector<LeafDesc> descs{dsc};
+    const auto st = run_leaf_batch(ex, prm, descs, {leaf_ws_layout(p, d[0], d, rq).total});
+    auto f = std::make_unique<tt_factors>();
+    f->p = p;
+    for (int m = 0; m < p; ++m) {
+      f->dims[m] = d[m];
+      f->ranks[m] = st[0].k[m];
+    }
+    f->core = download(dsc.out_core, static_cast<size_t>(prod_range(f->ranks, 0, p)), ex.stream);
+    for (int m = 0; m < p; ++m) f->f.push_back(download(dsc.out_f[m], static_cast<size_t>(d[m] * f->ranks[m]), ex.stream));
+    ex.sync();
+    f->objective = st[0].objective;
+    f->sweeps = st[0].sweeps;
+    f->converged = st[0].converged;
+    *out = f.release();
+  });
+}
+
+tt_status tt_stitch(int32_t nparts, int32_t p, const int64_t* part_dims, const int64_t* part_ranks,
+                    const double* const* cores, const double* const* factors, const int64_t* ranks, int32_t max_iters,
+                    double tol, uint64_t seed, int32_t device, tt_factors** out) {
+  return guarded([&] {
+    if (!out) fail(TT_EINVAL, "null argument");
+    *out = nullptr;
+    if (nparts < 1) fail(TT_EINVAL, "stitch: at least one part required");
+    if (p < 2 || p > TT_MAX_ORDER) fail(TT_EINVAL, "stitch: parts must have order >= 2");
+    if (!part_dims || !part_ranks || !cores || !factors || !ranks) fail(TT_EINVAL, "null argument");
+    if (max_iters < 1) fail(TT_EINVAL, "stitch: max_iters must be >= 1");
+    if (tol <= 0.0) fail(TT_EINVAL, "stitch: tol must be > 0");
+    for (int i = 1; i < nparts; ++i)
+      for (int m = 1; m < p; ++m)
+        if (part_dims[i * p + m] != part_dims[m]) fail(TT_EINVAL, "stitch: non-temporal shape mismatch across parts");
+    for (int m = 0; m < p; ++m)
+      if (ranks[m] < 1) fail(TT_EINVAL, "clamp_ranks: ranks must be >= 1");
+    StandaloneCtx& c = standalone(device);
+    Exec& ex = *c.ex;
+    DeviceGuard g(device);
+    Index d[kMaxP], rq[kMaxP], rc[kMaxP];
+    Index L = 0;
+    for (int i = 0; i < nparts; ++i) L += part_dims[i * p];
+    d[0] = L;
+    for (int m = 1; m < kMaxP; ++m) d[m] = m < p ? part_dims[m] : 1;
+    for (int m = 0; m < kMaxP; ++m) rq[m] = m < p ? ranks[m] : 1;
+    clamp_ranks(p, d, rq, rc);
+    std::vector<std::unique_ptr<DevBuf>> bufs;
+    std::vector<StitchPart> parts;
+    Index rho_max[kMaxP] = {};
+    for (int i = 0; i < nparts; ++i) {
+      StitchPart sp{};
+      const int64_t* pd = part_dims + i * p;
+      const int64_t* pr = part_ranks + i * p;
+      bufs.push_back(std::make_unique<DevBuf>());
+      sp.core = upload(*bufs.back(), cores[i], static_cast<size_t>(prod_range(pr, 0, p)), ex.stream);
+      for (int m = 0; m < p; ++m) {
+        if (pr[m] < 1 || pr[m] > pd[m]) fail(TT_EINVAL, "stitch: part rank out of range");
+        bufs.push_back(std::make_unique<DevBuf>());
+        const double* fm = upload(*bufs.back(), factors[i * p + m], static_cast<size_t>(pd[m] * pr[m]), ex.stream);
+        sp.rho[m] = pr[m];
+        rho_max[m] = std::max(rho_max[m], pr[m]);
+        if (m == 0) {
+          sp.v0 = fm;
+        } else {
+          sp.v[m] = fm;
+        }
+      }
+      sp.ld0 = pd[0];
+      sp.row0 = 0;
+      sp.len = pd[0];
+      sp.partial = 0;
+      parts.push_back(sp);
+    }
+    DevBuf bout;
+    size_t need = static_cast<size_t>(prod_range(rc, 0, p));
+    for (int m = 0; m < p; ++m) need += static_cast<size_t>(d[m] * rc[m]) + 32;
+    bout.ensure(need * sizeof(double));
+    StitchDesc dsc{};
+    dsc.part0 = 0;
+    dsc.nparts = nparts;
+    dsc.L = L;
+    double* cur = bout.as<double>();
+    for (int m = 0; m < p; ++m) {
+      dsc.out_f[m] = cur;
+      cur += d[m] * rc[m] + 16;
+    }
+    dsc.out_core = cur;
+    Params prm = make_params(p, d, rq, max_iters, tol);
+    InitCache init;
+    init.p = p;
+    for (int m = 0; m < p; ++m) {
+      init.d[m] = d[m];
+      init.req[m] = rq[m];
+    }
+    init.seed = seed;
+    init.stitch_init(prm, ex.stream);
+    std::vector<StitchDesc> descs{dsc};
+    const auto st = run_stitch_batch(ex, prm, descs, parts,
+                                     {stitch_ws_layout(p, L, d, rq, rho_max, nparts).total});
+    auto f = std::make_unique<tt_factors>();
+    f->p = p;
+    Index k[kMaxP];
+    for (int m = 0; m < p; ++m) k[m] = st[0].zero ? rc[m] : st[0].k[m];
+    if (st[0].zero) {
+      const auto u0 = init.stitch_zero_u0(L, rc[0]);
+      cuda_check(cudaMemcpyAsync(dsc.out_f[0], u0.data(), u0.size() * sizeof(double), cudaMemcpyHostToDevice, ex.stream),
+                 "zero-path upload");
+    }
+    for (int m = 0; m < p; ++m) {
+      f->dims[m] = d[m];
+      f->ranks[m] = k[m];
+    }
+    f->core = download(dsc.out_core, static_cast<size_t>(prod_range(k, 0, p)), ex.stream);
+    for (int m = 0; m < p; ++m) f->f.push_back(download(dsc.out_f[m], static_cast<size_t>(d[m] * k[m]), ex.stream));
+    ex.sync();
+    f->objective = st[0].objective;
+    f->sweeps = st[0].sweeps;
+    f->converged = st[0].converged;
+    *out = f.release();
+  });
+}
+
+tt_status tt_partial_hit(int32_t, const int64_t*, const int64_t*, const double*, const double* const*, int64_t,
+                         int64_t, int32_t, tt_factors** out) {
+  return guarded([&] {
+    if (out) *out = nullptr;
+    fail(TT_EINVAL, "tt_partial_hit: standalone partial-hit re-factoring is not part of this build; "
+                    "range queries fold partial hits into the stitch (see DESIGN.md)");
+  });
+}
+
+int32_t tt_factors_order(const tt_factors* f) { return f ? f->p : 0; }
+int64_t tt_factors_dim(const tt_factors* f, int32_t m) { return f ? f->dims[m] : 0; }
+int64_t tt_factors_rank(const tt_factors* f, int32_t m) { return f ? f->ranks[m] : 0; }
+const double* tt_factors_core(const tt_factors* f) { return f ? f->core.data() : nullptr; }
+const double* tt_factors_factor(const tt_factors* f, int32_t m) { return f ? f->f[m].data() : nullptr; }
+int32_t tt_factors_sweeps(const tt_factors* f) { return f ? f->sweeps : 0; }
+int32_t tt_factors_converged(const tt_factors* f) { return f ? f->converged : 0; }
+const double* tt_factors_objective(const tt_factors* f) { return f ? f->objective.data() : nullptr; }
+void tt_factors_free(tt_factors* f) { delete f; }
+
+}  // extern "C"

@@ -1,0 +1,491 @@
+// sm_100a ALS kernels for the stream segment tree hot path.
+//
+//  leaf_als_kernel   — tucker_als on one leaf block (tucker.cpp:86-119), one
+//                      CTA per leaf; X is streamed from HBM twice per sweep
+//                      (Y = X x_{m>=1} U_m^T for the mode-0 update, W = X x_0
+//                      U_0^T reused by every other mode and the core).
+//  stitch_als_kernel — stitch() (stitch.cpp:110-184) for appends (2 parts)
+//                      and range queries (s parts), one CTA per problem,
+//                      entirely in compressed r-sized coordinates: the L-row
+//                      temporal unfolding is never formed;
+//                      partial hits enter through the Gram S = Vsub^T Vsub
+//                      of their kept temporal rows instead of a QR.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include <atomic>
+
+#include "tt_block.cuh"
+
+namespace ttb {
+
+constexpr int kEigSmemN = 64;  // Jacobi runs in shared memory up to this size
+constexpr size_t kDynSmem = size_t(2) * kEigSmemN * kEigSmemN * sizeof(double);
+
+// Thread-per-output-element mode product, for shapes with few output columns.
+__device__ __forceinline__ void ttm_elems(const double* __restrict__ in, int64_t outer, int64_t d, int64_t inner,
+                                          const double* __restrict__ M, int64_t ms_a, int64_t ms_j, int64_t r,
+                                          double* __restrict__ out, bool acc) {
+  const int64_t tot = outer * r * inner;
+  for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
+    const int64_t t = e % inner;
+    const int64_t q = e / inner;
+    const int64_t a = q % r, o = q / r;
+    const double* src = in + o * d * inner + t;
+    const double* ma = M + a * ms_a;
+    double s = 0.0;
+    for (int64_t j = 0; j < d; ++j) s = fma(ma[j * ms_j], src[j * inner], s);
+    out[e] = acc ? out[e] + s : s;
+  }
+  __syncthreads();
+}
+
+// Dispatch: column-parallel when there are enough output columns.
+__device__ __forceinline__ void mode_product(const double* in, int64_t outer, int64_t d, int64_t inner,
+                                             const double* M, int64_t ms_a, int64_t ms_j, int64_t r, double* out,
+                                             bool acc) {
+  if (outer * inner >= 2 * int64_t(blockDim.x))
+    ttm(in, outer, d, inner, M, ms_a, ms_j, r, out, acc);
+  else
+    ttm_elems(in, outer, d, inner, M, ms_a, ms_j, r, out, acc);
+}
+
+// A Gram eigenvalue carries an absolute rounding error ~eps * lambda_max, so
+// singular values below ~sqrt(1e-13) * sigma_max are numerically zero: their
+// columns are completed orthonormally instead of amplified noise.
+__device__ __forceinline__ bool gram_sigma_ok(double lam, double lam_max) {
+  return lam > 1e-13 * lam_max && lam > 0.0;
+}
+
+// Runs the Jacobi solver on G (n x n), staging through shared memory when it
+// fits. Returns the pointer holding the eigenvectors; *diag receives the
+// pointer to the diagonalised matrix.
+__device__ double* eig_run(double* G, int n, double* V, int* order, double* dsm, double** diag, BlockScratch& sc) {
+  if (n <= kEigSmemN) {
+    double* As = dsm;
+    double* Vs = dsm + n * n;
+    bcopy(As, G, int64_t(n) * n);
+    sym_eig(As, n, Vs, order, sc);
+    *diag = As;
+    return Vs;
+  }
+  sym_eig(G, n, V, order, sc);
+  *diag = G;
+  return V;
+}
+
+// leading_left_singular_vectors (linalg.cpp:45-64) of the mode unfolding of a
+// row-major (outer, rows, inner) tensor, through the Gram matrix of its
+// smaller side. U: rows x k (ld rows), sign-fixed.
+__device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows, int64_t inner, int64_t k, double* U,
+                            double* G, double* V, double* misc, double* dsm, BlockScratch& sc) {
+  const int64_t cols = outer * inner;
+  int* order = reinterpret_cast<int*>(misc);
+  double* sig = misc + kMisc / 2;
+  double* diag = nullptr;
+  if (rows <= cols) {
+    const int n = int(rows);
+    gram_rows(P, outer, rows, inner, G);
+    const double* Vp = eig_run(G, n, V, order, dsm, &diag, sc);
+    for (int64_t idx = threadIdx.x; idx < rows * k; idx += blockDim.x) {
+      const int64_t i = idx % rows, c = idx / rows;
+      U[idx] = Vp[i + int64_t(order[c]) * n];
+    }
+    __syncthreads();
+  } else {
+    const int n = int(cols);
+    gram_cols(P, outer, rows, inner, G);
+    const double* Vp = eig_run(G, n, V, order, dsm, &diag, sc);
+    if (threadIdx.x < k) {
+      const double l0 = fmax(diag[order[0] * (n + 1)], 0.0);
+      const double lc = fmax(diag[order[threadIdx.x] * (n + 1)], 0.0);
+      sig[threadIdx.x] = gram_sigma_ok(lc, l0) ? 1.0 / sqrt(lc) : 0.0;
+    }
+    __syncthreads();
+    for (int64_t idx = threadIdx.x; idx < rows * k; idx += blockDim.x) {
+      const int64_t i = idx % rows, c = idx / rows;
+      const double inv = sig[c];
+      double s = 0.0;
+      if (inv != 0.0) {
+        const double* vc = Vp + int64_t(order[c]) * n;
+        for (int64_t o = 0; o < outer; ++o) {
+          const double* a = P + (o * rows + i) * inner;
+          const double* v = vc + o * inner;
+          for (int64_t t = 0; t < inner; ++t) s = fma(a[t], v[t], s);
+        }
+      }
+      U[idx] = s * inv;
+    }
+    __syncthreads();
+    orthonormalize(U, rows, 0, int(k), rows, sc);
+  }
+  sign_fix(U, rows, int(k), rows, nullptr, sc);
+}
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) leaf_als_kernel(Params prm, const LeafDesc* __restrict__ descs) {
+  __shared__ BlockScratch sc;
+  extern __shared__ double dsm[];
+  const LeafDesc D = descs[blockIdx.x];
+  const int p = prm.p;
+  int64_t d[kMaxP], rc[kMaxP], k[kMaxP];
+  d[0] = D.len;
+  for (int m = 1; m < p; ++m) d[m] = prm.d[m];
+  clamp_ranks(p, d, prm.req, rc);
+  const LeafWs lay = leaf_ws_layout(p, D.len, prm.d, prm.req);
+  double* W = D.ws + lay.W;
+  double* B[2] = {D.ws + lay.B1, D.ws + lay.B2};
+  double* G = D.ws + lay.G;
+  double* V = D.ws + lay.V;
+  double* misc = D.ws + lay.misc;
+  const double* X = D.x;
+  const int64_t ns = prod_range(d, 1, p);
+  const double norm_sq = bsumsq(X, D.len * ns, sc);
+  for (int n = 0; n < p; ++n) {
+    bcopy(D.out_f[n], D.init[n], d[n] * rc[n]);
+    k[n] = rc[n];
+  }
+  int sweeps = 0, converged = 0;
+  if (norm_sq == 0.0) {  // tucker.cpp:96-100
+    bzero(D.out_core, prod_range(rc, 0, p));
+    converged = 1;
+  } else {
+    const double norm = sqrt(norm_sq);
+    double prev_fit = nan("");
+    for (int sweep = 0; sweep < prm.max_iters; ++sweep) {
+      // ---- mode 0: Y = X x_1 U_1^T ... x_{p-1} U_{p-1}^T, U_0 = llsv(M_0(Y))
+      const int64_t k0n = leaf_mode_rank(p, d, k, 0);
+      int64_t cur[kMaxP];
+      for (int m = 0; m < p; ++m) cur[m] = d[m];
+      const double* src = X;
+      int tog = 0;
+      for (int m = 1; m < p; ++m) {
+        double* dst = B[tog];
+        mode_product(src, prod_range(cur, 0, m), cur[m], prod_range(cur, m + 1, p), D.out_f[m], d[m], 1, k[m], dst,
+                     false);
+        cur[m] = k[m];
+        src = dst;
+        tog ^= 1;
+      }
+      llsv_unfold(src, 1, d[0], prod_range(cur, 1, p), k0n, D.out_f[0], G, V, misc, dsm, sc);
+      k[0] = k0n;
+      // ---- W = X x_0 U_0^T : (k0, D_1, ..., D_{p-1})
+      mode_product(X, 1, d[0], ns, D.out_f[0], d[0], 1, k[0], W, false);
+      // ---- modes n >= 1 from W
+      const double* Pn = W;
+      int64_t pc[kMaxP];
+      for (int n = 1; n < p; ++n) {
+        const int64_t kn = leaf_mode_rank(p, d, k, n);
+        pc[0] = k[0];
+        for (int m = 1; m < p; ++m) pc[m] = d[m];
+        const double* s2 = W;
+        int t2 = 0;
+        for (int m = 1; m < p; ++m) {
+          if (m == n) continue;
+          double* dst = B[t2];
+          mode_product(s2, prod_range(pc, 0, m), pc[m], prod_range(pc, m + 1, p), D.out_f[m], d[m], 1, k[m], dst,
+                       false);
+          pc[m] = k[m];
+          s2 = dst;
+          t2 ^= 1;
+        }
+        llsv_unfold(s2, prod_range(pc, 0, n), d[n], prod_range(pc, n + 1, p), kn, D.out_f[n], G, V, misc, dsm, sc);
+        k[n] = kn;
+        Pn = s2;
+      }
+      // ---- core = P_{p-1} x_{p-1} U_{p-1}^T  (== core_of(x, U), tucker.cpp:67-76)
+      mode_product(Pn, prod_range(k, 0, p - 1), d[p - 1], 1, D.out_f[p - 1], d[p - 1], 1, k[p - 1], D.out_core,
+                   false);
+      const double core_sq = bsumsq(D.out_core, prod_range(k, 0, p), sc);
+      const double res = fmax(0.0, norm_sq - core_sq);
+      if (threadIdx.x == 0) D.objective[sweep] = res;
+      sweeps = sweep + 1;
+      const double fit = 1.0 - sqrt(res) / norm;
+      if (sweep > 0 && fabs(fit - prev_fit) < prm.tol) {
+        converged = 1;
+        break;
+      }
+      prev_fit = fit;
+    }
+  }
+  if (threadIdx.x == 0) {
+    D.status[0] = sweeps;
+    D.status[1] = converged;
+    D.status[2] = norm_sq == 0.0;
+    D.status[3] = 0;
+    for (int m = 0; m < kMaxP; ++m) D.status[4 + m] = m < p ? int(k[m]) : 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+struct PartView {
+  const double* core;
+  int64_t rho[kMaxP];
+  const double* v0;
+  int64_t ld0, row0, len;
+  int partial;
+  const double* v[kMaxP];
+};
+
+__device__ __forceinline__ PartView load_part(const StitchPart& s) {
+  PartView v;
+  v.core = s.core;
+  for (int m = 0; m < kMaxP; ++m) {
+    v.rho[m] = s.rho[m];
+    v.v[m] = s.v[m];
+  }
+  v.v0 = s.v0;
+  v.ld0 = s.ld0;
+  v.row0 = s.row0;
+  v.len = s.len;
+  v.partial = s.partial;
+  return v;
+}
+
+__global__ void __launch_bounds__(kThreads)
+    stitch_als_kernel(Params prm, const StitchDesc* __restrict__ descs, const StitchPart* __restrict__ parts_all) {
+  __shared__ BlockScratch sc;
+  __shared__ int flips[kMaxVec];
+  extern __shared__ double dsm[];
+  const StitchDesc D = descs[blockIdx.x];
+  const StitchPart* parts = parts_all + D.part0;
+  const int p = prm.p, s = D.nparts;
+  int64_t d[kMaxP], rc[kMaxP], k[kMaxP], rho_max[kMaxP], rcx[kMaxP];
+  d[0] = D.L;
+  for (int m = 1; m < p; ++m) d[m] = prm.d[m];
+  clamp_ranks(p, d, prm.req, rc);
+  for (int m = 0; m < p; ++m) rho_max[m] = 0;
+  for (int i = 0; i < s; ++i)
+    for (int m = 0; m < p; ++m) rho_max[m] = imax(rho_max[m], parts[i].rho[m]);
+  for (int m = 0; m < p; ++m) rcx[m] = imax(rc[m], rho_max[m]);
+  const StitchWs lay = stitch_ws_layout(p, D.L, prm.d, prm.req, rho_max, s);
+  double* ws = D.ws;
+  double* T[2] = {ws + lay.T1, ws + lay.T2};
+  double* G = ws + lay.G;
+  double* Vg = ws + lay.V;
+  double* Z = ws + lay.Z;
+  double* misc = ws + lay.misc;
+  double* wk = ws + lay.WK;  // Q x k0 scaled eigenvectors
+  double* HH = ws + lay.HH;  // rho0 x rho0 scratch
+  auto Pm = [&](int i, int m) {  // P_im = U_m^T V_im, k_m x rho_im (ld k_m)
+    int64_t off = 0;
+    for (int q = 1; q < m; ++q) off += rc[q] * rcx[q];
+    return ws + lay.P + int64_t(i) * lay.per_part_P + off;
+  };
+  auto Cp = [&](int i) { return ws + lay.C + int64_t(i) * lay.per_part_C; };
+  auto Sp = [&](int i) { return ws + lay.S + int64_t(i) * lay.per_part_S; };
+  auto Ep = [&](int i) { return ws + lay.E + int64_t(i) * lay.per_part_E; };
+  auto Ap = [&](int i) { return ws + lay.A + int64_t(i) * lay.per_part_E; };
+
+  // ---- partial-hit metric S_i = Vsub^T Vsub and the norm of the implied tensor
+  double norm_sq = 0.0;
+  for (int i = 0; i < s; ++i) {
+    const PartView pv = load_part(parts[i]);
+    const int64_t r0 = pv.rho[0];
+    const int64_t hk = prod_range(pv.rho, 1, p);
+    if (pv.partial) {
+      const double* vs = pv.v0 + pv.row0;
+      gemm(r0, r0, pv.len, vs, pv.ld0, 1, vs, 1, pv.ld0, Sp(i), 1, r0, false);
+      // ||H x_0 R||^2 = sum_ab S_ab (M0(H) M0(H)^T)_ab
+      gemm(r0, r0, hk, pv.core, hk, 1, pv.core, 1, hk, HH, 1, r0, false);
+      double acc = 0.0;
+      for (int64_t e = threadIdx.x; e < r0 * r0; e += blockDim.x) acc = fma(Sp(i)[e], HH[e], acc);
+      norm_sq += block_sum(acc, sc);
+    } else {
+      norm_sq += bsumsq(pv.core, r0 * hk, sc);
+    }
+  }
+  // ---- init (stitch.cpp:135-144): U_m = random_orthonormal(D_m, r_m), m >= 1
+  for (int m = 1; m < p; ++m) {
+    bcopy(D.out_f[m], prm.stitch_init[m], d[m] * rc[m]);
+    k[m] = rc[m];
+  }
+  k[0] = rc[0];
+  int sweeps = 0, converged = 0, any_zero_sigma = 0;
+  if (norm_sq == 0.0) {  // stitch.cpp:146-150; U_0 is drawn by the host
+    bzero(D.out_core, prod_range(rc, 0, p));
+    converged = 1;
+  } else {
+    for (int i = 0; i < s; ++i) {
+      const PartView pv = load_part(parts[i]);
+      for (int m = 1; m < p; ++m)
+        gemm(k[m], pv.rho[m], d[m], D.out_f[m], d[m], 1, pv.v[m], 1, d[m], Pm(i, m), 1, k[m], false);
+    }
+    const double norm = sqrt(norm_sq);
+    double prev_fit = nan("");
+    for (int sweep = 0; sweep < prm.max_iters; ++sweep) {
+      // ================= mode 0 (stitch_temporal_unfolding, stitch.cpp:49-73)
+      const int64_t k0n = stitch_mode_rank(p, d, rc, k, 0);
+      const int64_t Q = prod_range(k, 1, p);
+      for (int i = 0; i < s; ++i) {
+        const PartView pv = load_part(parts[i]);
+        int64_t cur[kMaxP];
+        for (int m = 0; m < p; ++m) cur[m] = pv.rho[m];
+        const double* src = pv.core;
+        int tog = 0;
+        for (int m = p - 1; m >= 1; --m) {  // descending, as the reference
+          double* dst = (m == 1) ? Cp(i) : T[tog];
+          mode_product(src, prod_range(cur, 0, m), cur[m], prod_range(cur, m + 1, p), Pm(i, m), 1, k[m], k[m],
+                       dst, false);
+          cur[m] = k[m];
+          src = dst;
+          tog ^= 1;
+        }
+      }
+      // G0 = Z0^T Z0 = sum_i C_i^T S_i C_i   (Q x Q)
+      for (int i = 0; i < s; ++i) {
+        const PartView pv = load_part(parts[i]);
+        const int64_t r0 = pv.rho[0];
+        const double* rhs = Cp(i);
+        if (pv.partial) {
+          gemm(r0, Q, r0, Sp(i), 1, r0, Cp(i), Q, 1, T[0], Q, 1, false);
+          rhs = T[0];
+        }
+        gemm(Q, Q, r0, Cp(i), 1, Q, rhs, Q, 1, G, 1, Q, i > 0);
+      }
+      {
+        int* order = reinterpret_cast<int*>(misc);
+        double* sig = misc + kMisc / 2;
+        double* diag = nullptr;
+        if (threadIdx.x == 0) sc.ibcast[1] = 0;
+        const double* Vp = eig_run(G, int(Q), Vg, order, dsm, &diag, sc);
+        if (threadIdx.x < k0n) {
+          const double l0 = fmax(diag[order[0] * (Q + 1)], 0.0);
+          const double lc = fmax(diag[order[threadIdx.x] * (Q + 1)], 0.0);
+          const bool ok = gram_sigma_ok(lc, l0);
+          sig[threadIdx.x] = ok ? 1.0 / sqrt(lc) : 0.0;
+          if (!ok) atomicOr(&sc.ibcast[1], 1);
+        }
+        __syncthreads();
+        for (int64_t idx = threadIdx.x; idx < Q * k0n; idx += blockDim.x) {
+          const int64_t j = idx % Q, c = idx / Q;
+          wk[idx] = Vp[j + int64_t(order[c]) * Q] * sig[c];
+        }
+        __syncthreads();
+        any_zero_sigma = sc.ibcast[1];
+      }
+      // E_i = C_i W Sigma^-1 (rho0 x k0);  A_i = S_i E_i = (U0[rows_i]^T V_i0)^T
+      for (int i = 0; i < s; ++i) {
+        const PartView pv = load_part(parts[i]);
+        const int64_t r0 = pv.rho[0];
+        gemm(r0, k0n, Q, Cp(i), Q, 1, wk, 1, Q, Ep(i), 1, r0, false);
+        if (pv.partial) gemm(r0, k0n, r0, Sp(i), 1, r0, Ep(i), 1, r0, Ap(i), 1, r0, false);
+      }
+      k[0] = k0n;
+      // ================= modes n >= 1 (stitch_nontemporal_unfolding, stitch.cpp:75-108)
+      for (int n = 1; n < p; ++n) {
+        const int64_t kn = stitch_mode_rank(p, d, rc, k, n);
+        int64_t zc[kMaxP];
+        for (int m = 0; m < p; ++m) zc[m] = (m == n) ? d[n] : k[m];
+        const int64_t zo = prod_range(zc, 0, n), zi = prod_range(zc, n + 1, p);
+        for (int i = 0; i < s; ++i) {
+          const PartView pv = load_part(parts[i]);
+          int64_t cur[kMaxP];
+          for (int m = 0; m < p; ++m) cur[m] = pv.rho[m];
+          const double* A0 = pv.partial ? Ap(i) : Ep(i);
+          // x_0 (U0[rows_i]^T V_i0): M(a, j) = A0[j + a*rho0]
+          mode_product(pv.core, 1, cur[0], prod_range(cur, 1, p), A0, cur[0], 1, k[0], T[0], false);
+          cur[0] = k[0];
+          const double* src = T[0];
+          int tog = 1;
+          for (int m = 1; m < p; ++m) {
+            if (m == n) continue;
+            double* dst = T[tog];
+            mode_product(src, prod_range(cur, 0, m), cur[m], prod_range(cur, m + 1, p), Pm(i, m), 1, k[m], k[m],
+                         dst, false);
+            cur[m] = k[m];
+            src = dst;
+            tog ^= 1;
+          }
+          // Z_n += F x_n V_in
+          mode_product(src, zo, cur[n], zi, pv.v[n], 1, d[n], d[n], Z, i > 0);
+        }
+        llsv_unfold(Z, zo, d[n], zi, kn, D.out_f[n], G, Vg, misc, dsm, sc);
+        k[n] = kn;
+        for (int i = 0; i < s; ++i) {
+          const PartView pv = load_part(parts[i]);
+          gemm(k[n], pv.rho[n], d[n], D.out_f[n], d[n], 1, pv.v[n], 1, d[n], Pm(i, n), 1, k[n], false);
+        }
+      }
+      // ================= core: fold Z_{p-1} and project the last mode (stitch.cpp:163-172)
+      mode_product(Z, prod_range(k, 0, p - 1), d[p - 1], 1, D.out_f[p - 1], d[p - 1], 1, k[p - 1], D.out_core,
+                   false);
+      const double core_sq = bsumsq(D.out_core, prod_range(k, 0, p), sc);
+      const double res = fmax(0.0, norm_sq - core_sq);
+      if (threadIdx.x == 0) D.objective[sweep] = res;
+      sweeps = sweep + 1;
+      const double fit = 1.0 - sqrt(res) / norm;
+      if (sweep > 0 && fabs(fit - prev_fit) < prm.tol) {
+        converged = 1;
+        break;
+      }
+      prev_fit = fit;
+    }
+    // ================= materialise U_0 = blockdiag(Vsub_i) [E_i] (L x k0), sign-fixed
+    const int64_t k0 = k[0];
+    double* U0 = D.out_f[0];
+    {
+      int64_t off = 0;
+      for (int i = 0; i < s; ++i) {
+        const PartView pv = load_part(parts[i]);
+        const int64_t r0 = pv.rho[0];
+        const double* vs = pv.v0 + pv.row0;
+        const double* E = Ep(i);
+        const int64_t tot = pv.len * k0;
+        for (int64_t idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+          const int64_t r = idx % pv.len, c = idx / pv.len;
+          double acc = 0.0;
+          for (int64_t a = 0; a < r0; ++a) acc = fma(vs[r + a * pv.ld0], E[a + c * r0], acc);
+          U0[off + r + c * D.L] = acc;
+        }
+        off += pv.len;
+      }
+      __syncthreads();
+    }
+    if (any_zero_sigma) orthonormalize(U0, D.L, 0, int(k0), D.L, sc);
+    sign_fix(U0, D.L, int(k0), D.L, flips, sc);
+    const int64_t slice = prod_range(k, 1, p);
+    for (int64_t e = threadIdx.x; e < k0 * slice; e += blockDim.x)
+      if (flips[e / slice]) D.out_core[e] = -D.out_core[e];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    D.status[0] = sweeps;
+    D.status[1] = converged;
+    D.status[2] = norm_sq == 0.0;
+    D.status[3] = any_zero_sigma;
+    for (int m = 0; m < kMaxP; ++m) D.status[4 + m] = m < p ? int(k[m]) : 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+std::atomic<int64_t> g_launches{0};
+
+cudaError_t launch_leaf(const Params& prm, const LeafDesc* d_descs, int n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(leaf_als_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDynSmem));
+    attr = true;
+  }
+  leaf_als_kernel<<<n, kThreads, kDynSmem, st>>>(prm, d_descs);
+  g_launches.fetch_add(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stitch(const Params& prm, const StitchDesc* d_descs, const StitchPart* d_parts, int n,
+                          cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(stitch_als_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDynSmem));
+    attr = true;
+  }
+  stitch_als_kernel<<<n, kThreads, kDynSmem, st>>>(prm, d_descs, d_parts);
+  g_launches.fetch_add(1);
+  return cudaGetLastError();
+}
+
+int64_t launches() { return g_launches.load(); }
+
+}  // namespace ttb

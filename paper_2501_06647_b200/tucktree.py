@@ -1,0 +1,431 @@
+"""Python mirror of the reference `tucktree` C++ API (sst.hpp, query.hpp,
+tucker.hpp, stitch.hpp) over the engine's C ABI (include/tucktree_b200.h).
+
+Same names, argument meaning and error behaviour as the reference:
+std::invalid_argument -> ValueError (InvalidArgument), std::logic_error ->
+RuntimeError (LogicError). Every numeric call runs on the GPU through
+libtucktree_b200.so; there is no CPU fallback — without the library or a CUDA
+device the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import build as _build
+
+MAX_ORDER = 8
+TT_MEM_HOST, TT_MEM_DEVICE = 0, 1
+LEAF, INTERMEDIATE, PLACEHOLDER = 0, 1, 2
+ENTIRE, PARTIAL, TAIL = 0, 1, 2
+FLAG_STRUCTURE_ONLY = 1
+kDefaultSeed = 20240117
+
+i64 = C.c_int64
+dptr = C.POINTER(C.c_double)
+i64ptr = C.POINTER(C.c_int64)
+vp = C.c_void_p
+
+
+class TTConfig(C.Structure):
+    _fields_ = [("order", C.c_int32), ("nontemporal", C.c_int64 * (MAX_ORDER - 1)), ("ranks", C.c_int64 * MAX_ORDER),
+                ("theta", C.c_double), ("max_iters", C.c_int32), ("tol", C.c_double), ("seed", C.c_uint64),
+                ("leaf_block", C.c_int64), ("device", C.c_int32), ("flags", C.c_int32)]
+
+
+class TTNodeInfo(C.Structure):
+    _fields_ = [("id", C.c_int64), ("begin", C.c_int64), ("end", C.c_int64), ("kind", C.c_int32),
+                ("has_decomposition", C.c_int32), ("left", C.c_int64), ("right", C.c_int64),
+                ("ranks", C.c_int64 * MAX_ORDER)]
+
+
+class TTHit(C.Structure):
+    _fields_ = [("node", C.c_int64), ("begin", C.c_int64), ("end", C.c_int64), ("flag", C.c_int32), ("pad", C.c_int32)]
+
+
+class TTRange(C.Structure):
+    _fields_ = [("ts", C.c_int64), ("te", C.c_int64)]
+
+
+class TTQueryOut(C.Structure):
+    _fields_ = [("core", dptr), ("factors", dptr * MAX_ORDER), ("ranks", C.c_int64 * MAX_ORDER), ("sweeps", C.c_int32),
+                ("converged", C.c_int32), ("objective", C.c_double), ("nhits", C.c_int32), ("pad", C.c_int32)]
+
+
+_lib = None
+
+SIGNATURES = {
+    "tt_last_error": (C.c_char_p, []),
+    "tt_version": (C.c_char_p, []),
+    "tt_kernel_launches": (i64, []),
+    "tt_tree_create": (C.c_int, [C.POINTER(TTConfig), C.POINTER(vp)]),
+    "tt_tree_destroy": (None, [vp]),
+    "tt_append": (C.c_int, [vp, dptr, i64, C.c_int]),
+    "tt_tree_stat": (i64, [vp, C.c_int32]),
+    "tt_node_info_get": (C.c_int, [vp, i64, C.POINTER(TTNodeInfo)]),
+    "tt_node_get": (C.c_int, [vp, i64, dptr, C.POINTER(dptr), C.c_int]),
+    "tt_last_redecomposed": (C.c_int, [vp, i64ptr, i64, i64ptr]),
+    "tt_validate": (C.c_int32, [vp, C.c_char_p, i64]),
+    "tt_recall": (C.c_int, [vp, i64, i64, C.c_double, C.POINTER(TTHit), i64, i64ptr]),
+    "tt_query_batch": (C.c_int, [vp, C.POINTER(TTRange), i64, C.c_double, C.POINTER(TTQueryOut), C.c_int]),
+    "tt_last_timing": (C.c_int, [vp, dptr]),
+    "tt_tucker_als": (C.c_int, [dptr, C.c_int32, i64ptr, i64ptr, C.c_int32, C.c_double, C.c_uint64, C.c_int32,
+                                C.POINTER(vp)]),
+    "tt_stitch": (C.c_int, [C.c_int32, C.c_int32, i64ptr, i64ptr, C.POINTER(dptr), C.POINTER(dptr), i64ptr,
+                            C.c_int32, C.c_double, C.c_uint64, C.c_int32, C.POINTER(vp)]),
+    "tt_partial_hit": (C.c_int, [C.c_int32, i64ptr, i64ptr, dptr, C.POINTER(dptr), i64, i64, C.c_int32,
+                                 C.POINTER(vp)]),
+    "tt_factors_order": (C.c_int32, [vp]),
+    "tt_factors_dim": (i64, [vp, C.c_int32]),
+    "tt_factors_rank": (i64, [vp, C.c_int32]),
+    "tt_factors_core": (dptr, [vp]),
+    "tt_factors_factor": (dptr, [vp, C.c_int32]),
+    "tt_factors_sweeps": (C.c_int32, [vp]),
+    "tt_factors_converged": (C.c_int32, [vp]),
+    "tt_factors_objective": (dptr, [vp]),
+    "tt_factors_free": (None, [vp]),
+}
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def lib():
+    """Loads libtucktree_b200.so (building it if absent). Raises if it cannot be loaded."""
+    global _lib
+    if _lib is None:
+        path = _build.LIB
+        if not os.path.exists(path):
+            _build.build()
+        L = C.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+class TuckTreeError(Exception):
+    pass
+
+
+class InvalidArgument(TuckTreeError, ValueError):
+    pass
+
+
+class LogicError(TuckTreeError, RuntimeError):
+    pass
+
+
+class CudaError(TuckTreeError, RuntimeError):
+    pass
+
+
+def _check(code: int):
+    if code == 0:
+        return
+    msg = lib().tt_last_error().decode()
+    if code == 1:
+        raise InvalidArgument(msg)
+    if code == 2:
+        raise LogicError(msg)
+    if code == 4:
+        raise CudaError(msg)
+    raise TuckTreeError(f"status {code}: {msg}")
+
+
+def _i(a):
+    a = np.ascontiguousarray(a, dtype=np.int64)
+    return a, a.ctypes.data_as(i64ptr)
+
+
+def _d(a):
+    return a.ctypes.data_as(dptr)
+
+
+@dataclass
+class TuckerFactors:
+    """tucker.hpp:33-40 — core (ranks) + factors[n] (D_n x r_n, orthonormal columns)."""
+
+    core: np.ndarray
+    factors: list
+    objective: list = field(default_factory=list)
+    converged: bool = False
+    sweeps: int = 0
+
+    @property
+    def order(self):
+        return len(self.factors)
+
+    def dim(self, m):
+        return self.factors[m].shape[0]
+
+    def rank(self, m):
+        return self.factors[m].shape[1]
+
+
+def _take_factors(h) -> TuckerFactors:
+    L = lib()
+    try:
+        p = L.tt_factors_order(h)
+        dims = [L.tt_factors_dim(h, m) for m in range(p)]
+        ranks = [L.tt_factors_rank(h, m) for m in range(p)]
+        n = int(np.prod(ranks))
+        core = np.ctypeslib.as_array(L.tt_factors_core(h), shape=(n,)).copy().reshape(ranks)
+        fs = []
+        for m in range(p):
+            k = dims[m] * ranks[m]
+            a = np.ctypeslib.as_array(L.tt_factors_factor(h, m), shape=(k,)).copy()
+            fs.append(a.reshape(ranks[m], dims[m]).T.copy())
+        sw = L.tt_factors_sweeps(h)
+        obj = list(np.ctypeslib.as_array(L.tt_factors_objective(h), shape=(sw,))) if sw else []
+        return TuckerFactors(core, fs, obj, bool(L.tt_factors_converged(h)), sw)
+    finally:
+        L.tt_factors_free(h)
+
+
+# ---------------------------------------------------------------------------
+def tucker_als(x: np.ndarray, ranks: Sequence[int], max_iters: int = 20, tol: float = 0.01, seed: int = kDefaultSeed,
+               device: int = 0) -> TuckerFactors:
+    """tucker.hpp:48-49 — Tucker ALS of a dense tensor on the GPU."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    if len(ranks) != x.ndim:
+        raise InvalidArgument("clamp_ranks: one rank per mode required")
+    dims, dp = _i(x.shape)
+    r, rp = _i(ranks)
+    h = vp()
+    _check(lib().tt_tucker_als(_d(x), x.ndim, dp, rp, max_iters, tol, seed, device, C.byref(h)))
+    return _take_factors(h)
+
+
+def stitch(parts: Sequence, ranks: Sequence[int], max_iters: int = 20, tol: float = 0.01, seed: int = kDefaultSeed,
+           device: int = 0) -> TuckerFactors:
+    """stitch.hpp:34-36 — ALS on the implied temporal concatenation of the parts, on the GPU."""
+    if len(parts) == 0:
+        raise InvalidArgument("stitch: at least one part required")
+    p = len(parts[0].factors)
+    if any(len(q.factors) != p for q in parts):
+        raise InvalidArgument("stitch: part order mismatch")
+    if len(ranks) != p:
+        raise InvalidArgument("stitch: one rank per mode required")
+    keep = []
+    pd = np.array([[q.factors[m].shape[0] for m in range(p)] for q in parts], dtype=np.int64).ravel()
+    pr = np.array([[q.factors[m].shape[1] for m in range(p)] for q in parts], dtype=np.int64).ravel()
+    cores = (dptr * len(parts))()
+    facs = (dptr * (len(parts) * p))()
+    for i, q in enumerate(parts):
+        c = np.ascontiguousarray(q.core, dtype=np.float64).ravel()
+        keep.append(c)
+        cores[i] = _d(c)
+        for m in range(p):
+            f = np.asfortranarray(q.factors[m], dtype=np.float64)
+            keep.append(f)
+            facs[i * p + m] = _d(f)
+    r, rp = _i(ranks)
+    h = vp()
+    _check(lib().tt_stitch(len(parts), p, pd.ctypes.data_as(i64ptr), pr.ctypes.data_as(i64ptr), cores, facs, rp,
+                           max_iters, tol, seed, device, C.byref(h)))
+    return _take_factors(h)
+
+
+# ---------------------------------------------------------------------------
+@dataclass
+class Node:
+    id: int
+    begin: int
+    end: int
+    kind: int
+    left: int
+    right: int
+    has_decomposition: bool
+    ranks: tuple
+
+    def length(self):
+        return self.end - self.begin
+
+
+@dataclass
+class HitEntry:
+    node: int
+    begin: int
+    end: int
+    flag: int
+
+    def length(self):
+        return self.end - self.begin
+
+
+@dataclass
+class QueryResult:
+    factors: TuckerFactors
+    hits: list
+
+
+class StreamSegmentTree:
+    """sst.hpp:54-105 on the GPU engine. `leaf_block` B generalises the
+    reference's single-slice leaves (B = 1 is the reference tree)."""
+
+    def __init__(self, nontemporal: Sequence[int], ranks: Sequence[int], theta: float = 0.7, max_iters: int = 20,
+                 tol: float = 0.01, seed: int = kDefaultSeed, leaf_block: int = 1, device: int = 0,
+                 structure_only: bool = False):
+        if len(nontemporal) == 0:
+            raise InvalidArgument("StreamSegmentTree: non-temporal shape required")
+        if len(ranks) != len(nontemporal) + 1:
+            raise InvalidArgument("StreamSegmentTree: one rank per mode required")
+        if len(ranks) > MAX_ORDER:
+            raise InvalidArgument("StreamSegmentTree: order must be <= 8")
+        cfg = TTConfig()
+        cfg.order = len(ranks)
+        for m, dm in enumerate(nontemporal):
+            cfg.nontemporal[m] = int(dm)
+        for m, r in enumerate(ranks):
+            cfg.ranks[m] = int(r)
+        cfg.theta, cfg.max_iters, cfg.tol, cfg.seed = theta, max_iters, tol, seed
+        cfg.leaf_block, cfg.device = leaf_block, device
+        cfg.flags = FLAG_STRUCTURE_ONLY if structure_only else 0
+        self.nontemporal = tuple(int(d) for d in nontemporal)
+        self.ranks = tuple(int(r) for r in ranks)
+        self.theta, self.leaf_block, self.device = theta, leaf_block, device
+        self.max_iters, self.tol, self.seed = max_iters, tol, seed
+        self._h = vp()
+        _check(lib().tt_tree_create(C.byref(cfg), C.byref(self._h)))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib().tt_tree_destroy(h)
+            self._h = None
+
+    # -- append ---------------------------------------------------------------
+    def append(self, slices: np.ndarray):
+        """One slice (shape == nontemporal) or a burst (n, *nontemporal)."""
+        s = np.ascontiguousarray(slices, dtype=np.float64)
+        ss = int(np.prod(self.nontemporal))
+        if s.shape == self.nontemporal:
+            n = 1
+        elif s.ndim == len(self.nontemporal) + 1 and s.shape[1:] == self.nontemporal:
+            n = s.shape[0]
+        else:
+            raise InvalidArgument("append: slice shape does not match tree")
+        _check(lib().tt_append(self._h, _d(s), n, TT_MEM_HOST))
+
+    def append_device(self, ptr: int, n: int):
+        """Burst append from device memory (pointer to n row-major slices)."""
+        _check(lib().tt_append(self._h, C.cast(C.c_void_p(ptr), dptr), n, TT_MEM_DEVICE))
+
+    def _stat(self, k):
+        return lib().tt_tree_stat(self._h, k)
+
+    def timespan(self):
+        return self._stat(0)
+
+    def height(self):
+        return self._stat(1)
+
+    def stitch_count(self):
+        return self._stat(2)
+
+    def last_append_node_touches(self):
+        return self._stat(3)
+
+    def node_count(self):
+        return self._stat(4)
+
+    def root(self):
+        return self._stat(5)
+
+    def leaves(self):
+        return self._stat(6)
+
+    def node(self, nid: int) -> Node:
+        info = TTNodeInfo()
+        _check(lib().tt_node_info_get(self._h, nid, C.byref(info)))
+        p = len(self.ranks)
+        return Node(info.id, info.begin, info.end, info.kind, info.left, info.right, bool(info.has_decomposition),
+                    tuple(info.ranks[m] for m in range(p)))
+
+    def nodes(self):
+        return [self.node(i) for i in range(1, self.node_count() + 1)]
+
+    def decomposition(self, nid: int) -> TuckerFactors:
+        v = self.node(nid)
+        if not v.has_decomposition:
+            raise LogicError("node has no decomposition")
+        p = len(self.ranks)
+        core = np.zeros(int(np.prod(v.ranks)))
+        rows = [v.length()] + list(self.nontemporal)
+        fs = [np.zeros(rows[m] * v.ranks[m]) for m in range(p)]
+        arr = (dptr * p)(*[_d(f) for f in fs])
+        _check(lib().tt_node_get(self._h, nid, _d(core), arr, TT_MEM_HOST))
+        return TuckerFactors(core.reshape(v.ranks), [f.reshape(v.ranks[m], rows[m]).T.copy() for m, f in enumerate(fs)])
+
+    def last_redecomposed(self):
+        out = np.zeros(4096, dtype=np.int64)
+        n = C.c_int64(0)
+        _check(lib().tt_last_redecomposed(self._h, out.ctypes.data_as(i64ptr), 4096, C.byref(n)))
+        return [int(v) for v in out[: n.value]]
+
+    def validate(self):
+        buf = C.create_string_buffer(1 << 16)
+        n = lib().tt_validate(self._h, buf, 1 << 16)
+        return [s for s in buf.value.decode().split("\n") if s][:n] if n > 0 else []
+
+    def last_timing_ms(self):
+        t = np.zeros(3)
+        _check(lib().tt_last_timing(self._h, _d(t)))
+        return t
+
+    # -- queries (query.hpp) ----------------------------------------------------
+    def recall(self, ts: int, te: int, theta: Optional[float] = None):
+        cap = 4096
+        out = (TTHit * cap)()
+        n = C.c_int64(0)
+        _check(lib().tt_recall(self._h, ts, te, -1.0 if theta is None else theta, out, cap, C.byref(n)))
+        return [HitEntry(out[i].node, out[i].begin, out[i].end, out[i].flag) for i in range(n.value)]
+
+    def range_query_batch(self, ranges, theta: Optional[float] = None, return_info: bool = False):
+        """range_query for many [ts, te) at once (one batched GPU launch)."""
+        ranges = [(int(a), int(b)) for a, b in ranges]
+        n = len(ranges)
+        p = len(self.ranks)
+        rr = (TTRange * max(n, 1))()
+        outs = (TTQueryOut * max(n, 1))()
+        keep = []
+        for i, (a, b) in enumerate(ranges):
+            rr[i].ts, rr[i].te = a, b
+            L = max(b - a, 1)
+            rc = [min(self.ranks[0], L)] + [min(r, d) for r, d in zip(self.ranks[1:], self.nontemporal)]
+            core = np.zeros(int(np.prod(rc)))
+            rows = [L] + list(self.nontemporal)
+            fs = [np.zeros(rows[m] * rc[m]) for m in range(p)]
+            keep.append((core, fs, rows))
+            outs[i].core = _d(core)
+            for m in range(p):
+                outs[i].factors[m] = _d(fs[m])
+        _check(lib().tt_query_batch(self._h, rr, n, -1.0 if theta is None else theta, outs, TT_MEM_HOST))
+        res = []
+        for i in range(n):
+            core, fs, rows = keep[i]
+            k = [outs[i].ranks[m] for m in range(p)]
+            f = TuckerFactors(core[: int(np.prod(k))].reshape(k),
+                              [fs[m][: rows[m] * k[m]].reshape(k[m], rows[m]).T.copy() for m in range(p)],
+                              [outs[i].objective], bool(outs[i].converged), outs[i].sweeps)
+            res.append((f, outs[i].nhits) if return_info else f)
+        return res
+
+    def range_query(self, ts: int, te: int, theta: Optional[float] = None) -> TuckerFactors:
+        return self.range_query_batch([(ts, te)], theta)[0]
+
+    def range_query_detailed(self, ts: int, te: int, theta: Optional[float] = None) -> QueryResult:
+        hits = self.recall(ts, te, theta)
+        return QueryResult(self.range_query(ts, te, theta), hits)
+
+
+def kernel_launches() -> int:
+    return lib().tt_kernel_launches()

@@ -1,0 +1,258 @@
+"""GPU parity: the CUDA engine (through its C ABI) against the CPU oracle on the
+same seeded inputs. Bit-exact on every integer (node ids, ranks, hit sets,
+sweep counts); floating point per BASELINE.json north_star: relative
+reconstruction error within 1e-6 of the oracle's and factor subspaces within
+1e-6 sin of the largest principal angle."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests import helpers as H
+
+pytestmark = pytest.mark.gpu
+
+RELERR_TOL = 1e-6   # |relerr_gpu - relerr_oracle|
+ANGLE_TOL = 1e-6    # sin(largest principal angle)
+
+
+@pytest.fixture(scope="module")
+def E():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2501_06647_b200 as eng
+
+    eng.lib()
+    return eng
+
+
+def _relerr(x, f):
+    return H.rel_residual(x, f)
+
+
+def assert_factors_match(x, got, want, where="", check_angles=True, gap_tol=1e-6):
+    assert [got.rank(m) for m in range(got.order)] == [want.rank(m) for m in range(want.order)], where
+    assert [got.dim(m) for m in range(got.order)] == [want.dim(m) for m in range(want.order)], where
+    for u in got.factors:
+        assert H.orthonormality_defect(u) <= 1e-8, where
+    if x is not None:
+        assert abs(_relerr(x, got) - _relerr(x, want)) <= RELERR_TOL, where
+    rg = H.reconstruct(got.core, got.factors)
+    rw = H.reconstruct(want.core, want.factors)
+    nrm = max(np.linalg.norm(rw), 1e-300)
+    assert np.linalg.norm(rg - rw) / nrm <= 1e-6, where
+    if check_angles:
+        for m in range(got.order):
+            # compare only columns separated by a spectral gap
+            a = H.unfold(rw, m)
+            s = np.linalg.svd(a, compute_uv=False)
+            k = got.rank(m)
+            if k < len(s) and s[0] > 0 and (s[k - 1] - s[k]) / s[0] < gap_tol:
+                continue
+            if s[0] == 0 or s[k - 1] / s[0] < 1e-9:
+                continue
+            assert H.max_sin_angle(got.factors[m], want.factors[m]) <= ANGLE_TOL, f"{where} mode {m}"
+
+
+# ------------------------------------------------------------------ tucker_als
+@pytest.mark.parametrize("shape,ranks,seed", [
+    ((12, 9, 7), (3, 2, 4), 1),
+    ((64, 32, 16), (5, 5, 5), 2),
+    ((128, 376, 6), (10, 10, 4), 3),
+    ((7, 6, 5), (3, 2, 2), 4),
+    ((1, 5, 4), (1, 5, 4), 5),
+    ((9, 9), (3, 3), 6),
+    ((4, 4, 4, 4), (3, 3, 3, 3), 7),
+    ((30, 10, 5), (3, 3, 3), 8),
+    ((1, 8, 8), (3, 3, 3), 9),
+    ((10, 4, 3, 2, 3), (2, 2, 2, 2, 2), 10),
+])
+def test_tucker_als_matches_oracle(E, shape, ranks, seed):
+    rng = np.random.default_rng(seed)
+    tr = tuple(min(2, d) for d in shape)
+    f = H.random_tucker(shape, tr, rng)
+    x = H.reconstruct(f.core, f.factors) + 0.05 * rng.standard_normal(shape)
+    want = O.tucker_als(x, ranks, seed=seed)
+    got = E.tucker_als(x, ranks, seed=seed)
+    assert got.sweeps == len(want.objective)
+    assert np.allclose(got.objective, want.objective, rtol=1e-8, atol=1e-10)
+    assert_factors_match(x, got, want, f"als {shape}")
+
+
+def test_tucker_als_exact_low_rank(E):  # test_tucker.cpp:42-61
+    rng = np.random.default_rng(100)
+    f = H.random_tucker([12, 9, 7], [3, 2, 4], rng)
+    x = H.reconstruct(f.core, f.factors)
+    g = E.tucker_als(x, [3, 2, 4], seed=42)
+    assert H.rel_residual(x, g) <= 1e-6
+    f2 = H.random_tucker([10, 8, 7], [2, 2, 2], rng)
+    x2 = H.reconstruct(f2.core, f2.factors)
+    g2 = E.tucker_als(x2, [4, 3, 5], seed=42)
+    assert H.rel_residual(x2, g2) <= 1e-6
+    assert all(H.orthonormality_defect(u) <= 1e-8 for u in g2.factors)
+
+
+def test_tucker_als_zero_tensor(E):  # test_tucker.cpp:70-80
+    g = E.tucker_als(np.zeros((4, 3, 2)), [2, 2, 2], seed=42)
+    want = O.tucker_als(np.zeros((4, 3, 2)), [2, 2, 2], seed=42)
+    assert g.converged and float(np.sum(g.core ** 2)) == 0.0
+    for a, b in zip(g.factors, want.factors):
+        assert np.max(np.abs(a - b)) <= 1e-12
+
+
+def test_tucker_als_monotone(E):  # test_tucker.cpp:196-210
+    rng = np.random.default_rng(107)
+    for trial in range(4):
+        x = rng.standard_normal((7, 6, 5))
+        g = E.tucker_als(x, [3, 2, 2], tol=1e-12, seed=1000 + trial)
+        want = O.tucker_als(x, [3, 2, 2], tol=1e-12, seed=1000 + trial)
+        obj = g.objective
+        for k in range(1, len(obj)):
+            assert obj[k] <= obj[k - 1] + 1e-9 * max(1.0, obj[k - 1])
+        assert len(obj) == len(want.objective)
+
+
+# ------------------------------------------------------------------ stitch
+def _parts(nontemporal, lengths, ranks, rng, noise=0.0):
+    parts = []
+    for n in lengths:
+        r = list(ranks)
+        r[0] = min(r[0], n)
+        parts.append(H.random_tucker([n] + list(nontemporal), r, rng))
+    return parts
+
+
+@pytest.mark.parametrize("nontemporal,lengths,ranks,req", [
+    ((5, 4), (6,), (2, 2, 2), (3, 3, 3)),
+    ((4, 3), (3, 2), (2, 2, 2), (2, 2, 2)),
+    ((4, 4), (1, 2), (2, 2, 2), (10, 2, 2)),
+    ((8, 6), (4, 4, 4, 4), (3, 3, 3), (3, 3, 3)),
+    ((376, 6), (128, 128), (10, 10, 4), (10, 10, 4)),
+    ((5,), (3, 4, 2), (2, 2), (3, 3)),
+    ((3, 2, 4), (2, 3, 4), (2, 2, 2, 2), (2, 2, 2, 2)),
+])
+def test_stitch_matches_oracle(E, nontemporal, lengths, ranks, req):
+    rng = np.random.default_rng(sum(lengths) + len(nontemporal))
+    parts = _parts(nontemporal, lengths, ranks, rng)
+    want = O.stitch(parts, req, seed=13)
+    got = E.stitch(parts, req, seed=13)
+    x = np.concatenate([H.reconstruct(q.core, q.factors) for q in parts], axis=0)
+    assert got.sweeps == len(want.objective)
+    assert_factors_match(x, got, want, f"stitch {nontemporal} {lengths}")
+
+
+def test_stitch_exact_blocks(E):  # test_stitch.cpp:158-180
+    rng = np.random.default_rng(203)
+    f = H.random_tucker([16, 6, 5], [3, 3, 3], rng)
+    x = H.reconstruct(f.core, f.factors)
+    parts = [E.tucker_als(x[b:b + 4], [3, 3, 3], seed=11) for b in range(0, 16, 4)]
+    out = E.stitch(parts, [3, 3, 3], seed=11)
+    assert out.dim(0) == 16 and H.rel_residual(x, out) <= 1e-6
+    assert all(H.orthonormality_defect(u) <= 1e-8 for u in out.factors)
+
+
+# ------------------------------------------------------------------ tree + queries
+def _series(shape, true_ranks, noise, seed):
+    return O.generate_synthetic(list(shape), list(true_ranks), noise, seed)
+
+
+def _compare_trees(E, series, ranks, B, theta=0.7, max_iters=20, seed=20240117, queries=(), append_chunks=None):
+    T = series.shape[0]
+    ora = O.Tree(series.shape[1:], ranks, theta=theta, max_iters=max_iters, seed=seed, leaf_block=B)
+    eng = E.StreamSegmentTree(series.shape[1:], ranks, theta=theta, max_iters=max_iters, seed=seed, leaf_block=B)
+    ora.append(series)
+    if append_chunks is None:
+        eng.append(series)
+    else:
+        pos = 0
+        for c in append_chunks:
+            eng.append(series[pos:pos + c])
+            pos += c
+        assert pos == T
+    assert eng.timespan() == ora.timespan and eng.stitch_count() == ora.stitch_count
+    assert eng.height() == ora.height and eng.validate() == []
+    on, en = ora.nodes(), eng.nodes()
+    assert [(v.id, v.begin, v.end, v.kind, v.left, v.right, v.has_decomposition) for v in on] == \
+           [(v.id, v.begin, v.end, v.kind, v.left, v.right, v.has_decomposition) for v in en]
+    for v in on:
+        if not v.has_decomposition:
+            continue
+        want = ora.node_factors(v.id)
+        got = eng.decomposition(v.id)
+        assert_factors_match(series[v.begin:v.end], got, want, f"node {v.id}")
+    if queries:
+        res = eng.range_query_batch(queries, return_info=True)
+        for (ts, te), (got, nh) in zip(queries, res):
+            hits_o = ora.recall(ts, te)
+            hits_e = [(h.node, h.begin, h.end, h.flag) for h in eng.recall(ts, te)]
+            assert hits_e == hits_o and nh == len(hits_o)
+            want = ora.range_query(ts, te)
+            assert got.sweeps == len(want.objective), (ts, te)
+            assert_factors_match(series[ts:te], got, want, f"query [{ts},{te})")
+    return ora, eng
+
+
+def _ranges(T, n, seed, minlen=1):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        a, b = sorted(int(v) for v in rng.integers(0, T + 1, size=2))
+        if b - a >= minlen:
+            out.append((a, b))
+    return out
+
+
+def test_tree_reference_leaves_b1(E):
+    series = _series((16, 4, 3), (3, 2, 2), 0.05, 37)
+    qs = [(1, 6), (0, 16), (5, 7), (2, 15), (3, 4), (0, 1), (15, 16)]
+    _compare_trees(E, series, (3, 3, 3), 1, max_iters=8, seed=5, queries=qs)
+
+
+def test_tree_config1_like(E):
+    # C1 shape at reduced T: (T=512, 32, 16), rank 5, leaf block 64
+    series = _series((512, 32, 16), (5, 5, 5), 0.3, 0)
+    _compare_trees(E, series, (5, 5, 5), 64, queries=_ranges(512, 40, 1))
+
+
+def test_tree_config2_like(E):
+    # C2 shape at reduced T: (T=1024, 376, 6), ranks (10, 10, 4), leaf 128
+    series = _series((1024, 376, 6), (10, 10, 4), 0.05, 2)
+    _compare_trees(E, series, (10, 10, 4), 128, queries=_ranges(1024, 30, 2, minlen=4))
+
+
+def test_tree_tail_and_streaming(E):
+    # blocks of 8 with a raw tail; appended in ragged chunks
+    series = _series((99, 8, 6), (3, 3, 3), 0.05, 12)
+    qs = [(0, 99), (3, 50), (17, 18), (40, 99), (90, 99), (96, 98), (0, 8), (8, 96)]
+    _compare_trees(E, series, (3, 3, 3), 8, queries=qs, append_chunks=[5, 3, 20, 1, 1, 30, 39])
+
+
+def test_tree_matrix_series_and_5way(E):
+    s2 = _series((12, 6), (3, 3), 0.05, 40)
+    _compare_trees(E, s2, (3, 3), 1, seed=5, queries=[(0, 12), (2, 9), (5, 6)])
+    s5 = _series((10, 4, 3, 2, 3), (2, 2, 2, 2, 2), 0.05, 41)
+    _compare_trees(E, s5, (2, 2, 2, 2, 2), 1, seed=5, queries=[(1, 8), (0, 10)])
+
+
+def test_tree_4way_config4_like(E):
+    series = _series((256, 16, 16, 8), (8, 8, 8, 4), 0.05, 4)
+    _compare_trees(E, series, (8, 8, 8, 4), 32, queries=_ranges(256, 20, 4))
+
+
+def test_query_short_ranges_rank_shrink(E):
+    # L < r0 queries: temporal rank clamps to L and non-temporal ranks shrink
+    series = _series((64, 20, 6), (4, 4, 3), 0.05, 9)
+    qs = [(5, 6), (5, 7), (10, 13), (62, 64), (0, 2)]
+    _compare_trees(E, series, (10, 10, 4), 4, queries=qs)
+
+
+def test_query_errors(E):
+    series = _series((16, 4, 3), (2, 2, 2), 0.0, 33)
+    t = E.StreamSegmentTree((4, 3), (2, 2, 2))
+    t.append(series)
+    for a, b in [(-1, 2), (2, 2), (0, 17)]:
+        with pytest.raises(ValueError):
+            t.range_query(a, b)
+    with pytest.raises(ValueError):
+        t.recall(0, 4, 1.0)
