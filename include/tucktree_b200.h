@@ -157,7 +157,8 @@ tt_status tt_last_redecomposed(const tt_tree* tree, int64_t* ids, int64_t cap, i
 int32_t tt_validate(const tt_tree* tree, char* buf, int64_t cap);
 
 /* ---- queries (query.hpp:33-50) -------------------------------------------- */
-/* recall(tree, ts, te, theta); theta <= 0 selects the tree's theta.        */
+/* recall(tree, ts, te, theta); theta = NaN selects the tree's theta
+ * (std::nullopt in the reference).                                          */
 tt_status tt_recall(const tt_tree* tree, int64_t ts, int64_t te, double theta, tt_hit* out, int64_t cap,
                     int64_t* n);
 

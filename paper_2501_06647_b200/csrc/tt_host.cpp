@@ -653,7 +653,7 @@ void collect_hits(const tt_tree& t, Index id, Index ts, Index te, double theta, 
 
 std::vector<tt_hit> recall(const tt_tree& t, Index ts, Index te, double theta_in) {  // query.cpp:35-47
   if (ts < 0 || ts >= te || te > t.timespan) fail(TT_EINVAL, "recall: query range must satisfy 0 <= ts < te <= T");
-  const double theta = theta_in > 0.0 ? theta_in : t.cfg.theta;
+  const double theta = std::isnan(theta_in) ? t.cfg.theta : theta_in;
   if (!(theta > 0.0 && theta < 1.0)) fail(TT_EINVAL, "recall: theta must be in (0, 1)");
   std::vector<tt_hit> out;
   const Index tb = t.leaves * t.B;

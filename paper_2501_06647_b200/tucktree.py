@@ -386,7 +386,7 @@ class StreamSegmentTree:
         cap = 4096
         out = (TTHit * cap)()
         n = C.c_int64(0)
-        _check(lib().tt_recall(self._h, ts, te, -1.0 if theta is None else theta, out, cap, C.byref(n)))
+        _check(lib().tt_recall(self._h, ts, te, float('nan') if theta is None else theta, out, cap, C.byref(n)))
         return [HitEntry(out[i].node, out[i].begin, out[i].end, out[i].flag) for i in range(n.value)]
 
     def range_query_batch(self, ranges, theta: Optional[float] = None, return_info: bool = False):
@@ -408,7 +408,7 @@ class StreamSegmentTree:
             outs[i].core = _d(core)
             for m in range(p):
                 outs[i].factors[m] = _d(fs[m])
-        _check(lib().tt_query_batch(self._h, rr, n, -1.0 if theta is None else theta, outs, TT_MEM_HOST))
+        _check(lib().tt_query_batch(self._h, rr, n, float('nan') if theta is None else theta, outs, TT_MEM_HOST))
         res = []
         for i in range(n):
             core, fs, rows = keep[i]
