@@ -165,11 +165,13 @@ def run_engine(args, rank, world, local_rank):
     hbuf, houts, _, _ = query_outputs(eng, w, ranges, host_alloc)
     nsteps = args.warmup + args.steps
     mk = lambda: eng.StreamSegmentTree(w.shape[1:], w.ranks, leaf_block=w.leaf_block, device=local_rank)
-    trees = [mk() for _ in range(nsteps)]
-    e2e_trees = [mk() for _ in range(nsteps)]
+    tree_v, tree_e = mk(), mk()  # each step clears and rebuilds (buffers kept: no allocation in the timed region)
+    trees = [tree_v] * nsteps
+    e2e_trees = [tree_e] * nsteps
     torch.cuda.synchronize()
 
     def step(tree, device_resident):
+        tree.clear()
         if device_resident:
             tree.append_device(xd.data_ptr(), T)
         else:
@@ -218,6 +220,7 @@ def run_engine(args, rank, world, local_rank):
     for i in range(args.warmup, nsteps):
         e0.record()
         tr = e2e_trees[i]
+        tr.clear()
         eng.tucktree._check(L.tt_append(tr._h, C.cast(C.c_void_p(xh.data_ptr()), eng.tucktree.dptr), T, 0))
         e1.record()
         eng.tucktree._check(L.tt_query_batch(tr._h, rr, nq, float("nan"), houts, 0))

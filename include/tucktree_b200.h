@@ -128,6 +128,11 @@ void tt_tree_destroy(tt_tree* tree);
  * level by level — result-identical to n sequential appends.  sst.hpp:64-67 */
 tt_status tt_append(tt_tree* tree, const double* slices, int64_t n, tt_mem where);
 
+/* Empties the tree (timespan 0, no nodes) but keeps its device buffers and
+ * init-factor caches, so a rebuild allocates nothing. Not in the reference
+ * API (equivalent to constructing a new StreamSegmentTree).               */
+tt_status tt_tree_clear(tt_tree* tree);
+
 /* timespan / height / stitch_count / last_append_node_touches / node_count /
  * root / leaves                                            sst.hpp:69-91 */
 enum {

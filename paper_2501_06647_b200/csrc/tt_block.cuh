@@ -121,16 +121,14 @@ __device__ __forceinline__ void ttm_chunk(const double* __restrict__ in, int64_t
 
 __device__ __forceinline__ void ttm(const double* in, int64_t outer, int64_t d, int64_t inner, const double* M,
                                     int64_t ms_a, int64_t ms_j, int64_t r, double* out, bool acc) {
-  for (int a0 = 0; a0 < r; a0 += 32) {
-    const int na = int(imin(32, r - a0));
+  for (int a0 = 0; a0 < r; a0 += 16) {
+    const int na = int(imin(16, r - a0));
     if (na <= 4)
       ttm_chunk<4>(in, outer, d, inner, M, ms_a, ms_j, a0, na, out, r, acc);
     else if (na <= 8)
       ttm_chunk<8>(in, outer, d, inner, M, ms_a, ms_j, a0, na, out, r, acc);
-    else if (na <= 16)
-      ttm_chunk<16>(in, outer, d, inner, M, ms_a, ms_j, a0, na, out, r, acc);
     else
-      ttm_chunk<32>(in, outer, d, inner, M, ms_a, ms_j, a0, na, out, r, acc);
+      ttm_chunk<16>(in, outer, d, inner, M, ms_a, ms_j, a0, na, out, r, acc);
   }
   __syncthreads();
 }
@@ -201,16 +199,25 @@ __device__ __forceinline__ void gram_cols(const double* __restrict__ P, int64_t 
 __device__ void sym_eig(double* A, int n, double* V, int* order, BlockScratch& sc) {
   const int n2 = n + (n & 1);
   const int np = n2 / 2;
-  for (int64_t i = threadIdx.x; i < int64_t(n) * n; i += blockDim.x) V[i] = (i % n == i / n) ? 1.0 : 0.0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = warp; j < n; j += kWarps)
+    for (int i = lane; i < n; i += 32) V[i + j * n] = (i == j) ? 1.0 : 0.0;
   if (threadIdx.x < 2) sc.rotated[threadIdx.x] = 0;
-  __syncthreads();
   if (n <= 1) {
     if (threadIdx.x == 0 && n == 1) order[0] = 0;
     __syncthreads();
     return;
   }
+  // Skip a rotation when |a_pq| <= max(eps_r sqrt(|a_pp a_qq|), eps_a ||A||_F):
+  // the relative test keeps the large eigenpairs accurate to working
+  // precision, the absolute floor stops the solver from chasing rounding noise
+  // between numerically-zero eigenvalues (eigenvector error <= eps_a/gap).
+  double fro = 0.0;
+  for (int j = warp; j < n; j += kWarps)
+    for (int i = lane; i < n; i += 32) fro = fma(A[i + j * n], A[i + j * n], fro);
+  const double abs_thr = 1e-16 * sqrt(block_sum(fro, sc));
   const double eps = 1e-15;
-  for (int sweep = 0; sweep < 30; ++sweep) {
+  for (int sweep = 0; sweep < 20; ++sweep) {
     const int cur = sweep & 1;
     if (threadIdx.x == 0) sc.rotated[cur ^ 1] = 0;
     for (int r = 0; r < n2 - 1; ++r) {
@@ -232,7 +239,7 @@ __device__ void sym_eig(double* A, int n, double* V, int* order, BlockScratch& s
         if (q < n) {
           const double apq = A[p + q * n];
           const double app = A[p + p * n], aqq = A[q + q * n];
-          if (apq != 0.0 && fabs(apq) > eps * sqrt(fabs(app)) * sqrt(fabs(aqq))) {
+          if (fabs(apq) > fmax(eps * sqrt(fabs(app)) * sqrt(fabs(aqq)), abs_thr)) {
             const double tau = (aqq - app) / (2.0 * apq);
             if (fabs(tau) > 1e150) {
               t = 0.5 / tau;
@@ -251,48 +258,53 @@ __device__ void sym_eig(double* A, int n, double* V, int* order, BlockScratch& s
         sc.jt[k] = t;
       }
       __syncthreads();
-      const int nb = np * np;
-      for (int idx = threadIdx.x; idx < nb; idx += blockDim.x) {
-        const int P1 = idx % np, P2 = idx / np;
-        const int p = sc.jp[P1], q = sc.jq[P1];
-        const double c = sc.jc[P1], s = sc.js[P1];
-        if (P1 == P2) {
-          if (s != 0.0) {
-            const double apq = A[p + q * n];
-            const double t = sc.jt[P1];
-            A[p + p * n] -= t * apq;
-            A[q + q * n] += t * apq;
-            A[p + q * n] = 0.0;
-            A[q + p * n] = 0.0;
-          }
-          continue;
-        }
+      // A <- J^T A J on 2x2 blocks (one owner thread per block), V <- V J.
+      for (int P2 = warp; P2 < np; P2 += kWarps) {
         const int p2 = sc.jp[P2], q2 = sc.jq[P2];
         const double c2 = sc.jc[P2], s2 = sc.js[P2];
-        if (s == 0.0 && s2 == 0.0) continue;
-        const bool hq = q < n, hq2 = q2 < n;
-        const double m00 = A[p + p2 * n];
-        const double m01 = hq2 ? A[p + q2 * n] : 0.0;
-        const double m10 = hq ? A[q + p2 * n] : 0.0;
-        const double m11 = (hq && hq2) ? A[q + q2 * n] : 0.0;
-        // X = J1^T M ; Y = X J2 with J = [[c, s], [-s, c]]
-        const double x00 = c * m00 - s * m10, x01 = c * m01 - s * m11;
-        const double x10 = s * m00 + c * m10, x11 = s * m01 + c * m11;
-        A[p + p2 * n] = c2 * x00 - s2 * x01;
-        if (hq2) A[p + q2 * n] = s2 * x00 + c2 * x01;
-        if (hq) A[q + p2 * n] = c2 * x10 - s2 * x11;
-        if (hq && hq2) A[q + q2 * n] = s2 * x10 + c2 * x11;
+        const bool hq2 = q2 < n;
+        for (int P1 = lane; P1 < np; P1 += 32) {
+          const double s1 = sc.js[P1];
+          if (P1 == P2) {
+            if (s1 != 0.0) {
+              const int p = sc.jp[P1], q = sc.jq[P1];
+              const double apq = A[p + q * n];
+              const double t = sc.jt[P1];
+              A[p + p * n] -= t * apq;
+              A[q + q * n] += t * apq;
+              A[p + q * n] = 0.0;
+              A[q + p * n] = 0.0;
+            }
+            continue;
+          }
+          if (s1 == 0.0 && s2 == 0.0) continue;
+          const int p = sc.jp[P1], q = sc.jq[P1];
+          const double c = sc.jc[P1];
+          const bool hq = q < n;
+          const double m00 = A[p + p2 * n];
+          const double m01 = hq2 ? A[p + q2 * n] : 0.0;
+          const double m10 = hq ? A[q + p2 * n] : 0.0;
+          const double m11 = (hq && hq2) ? A[q + q2 * n] : 0.0;
+          const double x00 = c * m00 - s1 * m10, x01 = c * m01 - s1 * m11;
+          const double x10 = s1 * m00 + c * m10, x11 = s1 * m01 + c * m11;
+          A[p + p2 * n] = c2 * x00 - s2 * x01;
+          if (hq2) A[p + q2 * n] = s2 * x00 + c2 * x01;
+          if (hq) A[q + p2 * n] = c2 * x10 - s2 * x11;
+          if (hq && hq2) A[q + q2 * n] = s2 * x10 + c2 * x11;
+        }
       }
-      const int nv = n * np;
-      for (int idx = threadIdx.x; idx < nv; idx += blockDim.x) {
-        const int i = idx % n, P1 = idx / n;
-        const double s = sc.js[P1];
-        if (s == 0.0) continue;
+      for (int P1 = warp; P1 < np; P1 += kWarps) {
+        const double s1 = sc.js[P1];
+        if (s1 == 0.0) continue;
         const int p = sc.jp[P1], q = sc.jq[P1];
         const double c = sc.jc[P1];
-        const double vp = V[i + p * n], vq = V[i + q * n];
-        V[i + p * n] = c * vp - s * vq;
-        V[i + q * n] = s * vp + c * vq;
+        double* vp = V + p * n;
+        double* vq = V + q * n;
+        for (int i = lane; i < n; i += 32) {
+          const double a = vp[i], b = vq[i];
+          vp[i] = c * a - s1 * b;
+          vq[i] = s1 * a + c * b;
+        }
       }
       __syncthreads();
     }

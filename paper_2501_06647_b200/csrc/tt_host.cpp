@@ -148,8 +148,9 @@ struct DevBuf {
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
-    cuda_check(cudaMalloc(&p, std::max<size_t>(b, 256)), "cudaMalloc");
-    bytes = std::max<size_t>(b, 256);
+    const size_t nb = std::max<size_t>(b + b / 4, 256);  // grow geometrically
+    cuda_check(cudaMalloc(&p, nb), "cudaMalloc");
+    bytes = nb;
   }
   template <class T>
   T* as() const {
@@ -159,21 +160,35 @@ struct DevBuf {
 
 // Bump allocator over large chunks for node decompositions (never moves).
 struct Arena {
-  std::vector<void*> chunks;
+  std::vector<std::pair<void*, size_t>> chunks;
+  size_t ci = 0;  // current chunk
   char* cur = nullptr;
   size_t left = 0;
   static constexpr size_t kChunk = size_t(256) << 20;
   ~Arena() {
-    for (void* c : chunks) cudaFree(c);
+    for (auto& c : chunks) cudaFree(c.first);
+  }
+  // Forget every allocation but keep the chunks for reuse (tt_tree_clear).
+  void reset() {
+    ci = 0;
+    cur = chunks.empty() ? nullptr : static_cast<char*>(chunks[0].first);
+    left = chunks.empty() ? 0 : chunks[0].second;
   }
   double* alloc(size_t n_doubles) {
     size_t b = (n_doubles * sizeof(double) + 255) & ~size_t(255);
     if (b == 0) b = 256;
-    if (b > left) {
+    while (b > left) {
+      if (cur != nullptr && ci + 1 < chunks.size()) {  // reuse the next kept chunk
+        ++ci;
+        cur = static_cast<char*>(chunks[ci].first);
+        left = chunks[ci].second;
+        continue;
+      }
       const size_t cb = std::max(kChunk, b);
       void* c = nullptr;
       cuda_check(cudaMalloc(&c, cb), "cudaMalloc(arena)");
-      chunks.push_back(c);
+      chunks.emplace_back(c, cb);
+      ci = chunks.size() - 1;
       cur = static_cast<char*>(c);
       left = cb;
     }
@@ -806,6 +821,16 @@ tt_status tt_append(tt_tree* t, const double* slices, int64_t n, tt_mem where) {
       t->ex->sync();
     }
     t->last_redec = all_redec;
+  });
+}
+
+tt_status tt_tree_clear(tt_tree* t) {
+  return guarded([&] {
+    if (!t) fail(TT_EINVAL, "null tree");
+    t->nodes.clear();
+    t->root = t->timespan = t->leaves = t->stitch_count = t->last_touches = 0;
+    t->last_redec.clear();
+    if (t->arena) t->arena->reset();
   });
 }
 

@@ -123,7 +123,7 @@ __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows, int64_
 }
 
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) leaf_als_kernel(Params prm, const LeafDesc* __restrict__ descs) {
+__global__ void __launch_bounds__(kThreads, 2) leaf_als_kernel(Params prm, const LeafDesc* __restrict__ descs) {
   __shared__ BlockScratch sc;
   extern __shared__ double dsm[];
   const LeafDesc D = descs[blockIdx.x];
@@ -242,7 +242,7 @@ __device__ __forceinline__ PartView load_part(const StitchPart& s) {
   return v;
 }
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 2)
     stitch_als_kernel(Params prm, const StitchDesc* __restrict__ descs, const StitchPart* __restrict__ parts_all) {
   __shared__ BlockScratch sc;
   __shared__ int flips[kMaxVec];

@@ -64,6 +64,7 @@ SIGNATURES = {
     "tt_kernel_launches": (i64, []),
     "tt_tree_create": (C.c_int, [C.POINTER(TTConfig), C.POINTER(vp)]),
     "tt_tree_destroy": (None, [vp]),
+    "tt_tree_clear": (C.c_int, [vp]),
     "tt_append": (C.c_int, [vp, dptr, i64, C.c_int]),
     "tt_tree_stat": (i64, [vp, C.c_int32]),
     "tt_node_info_get": (C.c_int, [vp, i64, C.POINTER(TTNodeInfo)]),
@@ -99,7 +100,7 @@ def lib():
     """Loads libtucktree_b200.so (building it if absent). Raises if it cannot be loaded."""
     global _lib
     if _lib is None:
-        path = _build.LIB
+        path = os.environ.get("TT_LIB_PATH") or _build.LIB
         if not os.path.exists(path):
             _build.build()
         L = C.CDLL(path)
@@ -318,6 +319,10 @@ class StreamSegmentTree:
     def append_device(self, ptr: int, n: int):
         """Burst append from device memory (pointer to n row-major slices)."""
         _check(lib().tt_append(self._h, C.cast(C.c_void_p(ptr), dptr), n, TT_MEM_DEVICE))
+
+    def clear(self):
+        """Empty the tree, keeping device buffers (a rebuild allocates nothing)."""
+        _check(lib().tt_tree_clear(self._h))
 
     def _stat(self, k):
         return lib().tt_tree_stat(self._h, k)
