@@ -189,6 +189,7 @@ def run_engine(args, rank, world, local_rank):
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = eng.kernel_launches()
+    stats0 = eng.solver_stats()
     t_app = t_q = t_leaf = t_stitch_build = t_stitch_q = 0.0
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -204,6 +205,8 @@ def run_engine(args, rank, world, local_rank):
         ev1.record()
         torch.cuda.synchronize()
     launches = eng.kernel_launches() - launches0
+    stats1 = eng.solver_stats()
+    solver = {k: (stats1[k] - stats0[k]) / args.steps for k in stats0}
     span_ms = ev0.elapsed_time(ev1)
     if dist:
         dist.barrier()
@@ -289,6 +292,7 @@ def run_engine(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(out_bytes), "append_slices_per_s": round(e2e_sps, 3)},
         "roofline": roof,
         "gpu_launches": int(launches),
+        "solver_per_step": solver,
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:

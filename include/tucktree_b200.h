@@ -206,6 +206,13 @@ void tt_factors_free(tt_factors* f);
  * reports the delta over its timed region).                               */
 int64_t tt_kernel_launches(void);
 
+/* Cumulative solver counters since process start (instrumentation):
+ * [0] ALS problems, [1] ALS sweeps, [2] eigen-solves, [3] Jacobi sweeps,
+ * [4..11] thousands of SM cycles summed over problems in: eigen-solves, Gram
+ * matrices (+U assembly), small mode products, small GEMMs, orthonormalise +
+ * sign fix, U_0 materialisation, leaf X passes, whole problem.            */
+void tt_solver_stats(int64_t* out12);
+
 #ifdef __cplusplus
 }
 #endif

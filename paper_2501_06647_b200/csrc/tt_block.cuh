@@ -28,7 +28,16 @@ struct BlockScratch {
   double jc[256], js[256], jt[256];
   int jp[256], jq[256];
   int rotated[2];
+  int eig_calls, eig_sweeps;  // instrumentation (Jacobi sweeps per problem)
+  long long cyc[8];           // instrumentation: cycles per phase (see kPhase*)
 };
+
+// Phase-timer slots (thread 0 accumulates clock64 deltas; instrumentation).
+enum { kPhEig = 0, kPhGram = 1, kPhTtm = 2, kPhGemm = 3, kPhOrtho = 4, kPhU0 = 5, kPhBig = 6, kPhAll = 7 };
+__device__ __forceinline__ long long tstart() { return threadIdx.x == 0 ? clock64() : 0; }
+__device__ __forceinline__ void tstop(BlockScratch& sc, int slot, long long t0) {
+  if (threadIdx.x == 0) sc.cyc[slot] += clock64() - t0;
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -133,11 +142,38 @@ __device__ __forceinline__ void ttm(const double* in, int64_t outer, int64_t d, 
   __syncthreads();
 }
 
-// C(i,j) (+)= alpha * sum_k A(i,k) B(k,j); element (i,j) of X at X[i*rs + j*cs].
+// C(i,j) (+)= sum_k A(i,k) B(k,j); element (i,j) of X at X[i*rs + j*cs].
+// Few outputs with a long K (e.g. V_sub^T V_sub over thousands of rows) split
+// K across the block and reduce the partials through shared memory.
 __device__ __forceinline__ void gemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t ars, int64_t acs,
                                      const double* B, int64_t brs, int64_t bcs, double* C, int64_t crs, int64_t ccs,
-                                     bool acc) {
+                                     bool acc, BlockScratch& sc) {
   const int64_t tot = M * N;
+  const int64_t split = (tot <= 128 && K >= 64) ? imin(int64_t(blockDim.x) / tot, K / 16) : 1;
+  if (split >= 2) {
+    const int64_t kc = (K + split - 1) / split;
+    const int64_t work = tot * split;
+    if (threadIdx.x < work) {
+      const int64_t e = threadIdx.x % tot, part = threadIdx.x / tot;
+      const int64_t i = e % M, j = e / M;
+      const int64_t k0 = part * kc, k1 = imin(K, k0 + kc);
+      const double* a = A + i * ars;
+      const double* b = B + j * bcs;
+      double s = 0.0;
+      for (int64_t k = k0; k < k1; ++k) s = fma(a[k * acs], b[k * brs], s);
+      sc.red[threadIdx.x] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < tot) {
+      const int64_t i = threadIdx.x % M, j = threadIdx.x / M;
+      double s = 0.0;
+      for (int64_t part = 0; part < split; ++part) s += sc.red[part * tot + threadIdx.x];
+      double* c = C + i * crs + j * ccs;
+      *c = acc ? *c + s : s;
+    }
+    __syncthreads();
+    return;
+  }
   for (int64_t idx = threadIdx.x; idx < tot; idx += blockDim.x) {
     const int64_t i = idx % M, j = idx / M;
     double s = 0.0;
@@ -146,6 +182,46 @@ __device__ __forceinline__ void gemm(int64_t M, int64_t N, int64_t K, const doub
     for (int64_t k = 0; k < K; ++k) s = fma(a[k * acs], b[k * brs], s);
     double* c = C + i * crs + j * ccs;
     *c = acc ? *c + s : s;
+  }
+  __syncthreads();
+}
+
+// G = V^T V for a tall column-major V (rows x k, ld), k small: warps own pair
+// groups (i <= j), lanes stride over rows, warp shuffles reduce.  G: k x k.
+__device__ __forceinline__ void gram_tall(const double* __restrict__ V, int64_t ld, int64_t rows, int k,
+                                          double* __restrict__ G) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = int(blockDim.x >> 5);
+  const int npairs = k * (k + 1) / 2;
+  constexpr int PB = 8;
+  for (int base = warp * PB; base < npairs; base += nw * PB) {
+    int pi[PB], pj[PB];
+#pragma unroll
+    for (int u = 0; u < PB; ++u) {
+      int e = base + u, i = 0;
+      if (e >= npairs) e = npairs - 1;
+      while (e >= k - i) {  // pair index -> (i, j) in the upper triangle, row-major
+        e -= k - i;
+        ++i;
+      }
+      pi[u] = i;
+      pj[u] = i + e;
+    }
+    double acc[PB];
+#pragma unroll
+    for (int u = 0; u < PB; ++u) acc[u] = 0.0;
+    for (int64_t r = lane; r < rows; r += 32) {
+#pragma unroll
+      for (int u = 0; u < PB; ++u) acc[u] = fma(V[r + pi[u] * ld], V[r + pj[u] * ld], acc[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < PB; ++u) {
+      const double v = warp_sum(acc[u]);
+      if (lane == 0 && base + u < npairs) {
+        G[pi[u] + pj[u] * k] = v;
+        G[pj[u] + pi[u] * k] = v;
+      }
+    }
   }
   __syncthreads();
 }
@@ -196,7 +272,7 @@ __device__ __forceinline__ void gram_cols(const double* __restrict__ P, int64_t 
 // (ties by lower index). One round rotates n/2 disjoint planes at once; each
 // 2x2 block of A and each row pair of V is owned by one thread, so a round is
 // two barriers.
-__device__ void sym_eig(double* A, int n, double* V, int* order, BlockScratch& sc) {
+__device__ int sym_eig(double* A, int n, double* V, int* order, BlockScratch& sc) {
   const int n2 = n + (n & 1);
   const int np = n2 / 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -206,7 +282,7 @@ __device__ void sym_eig(double* A, int n, double* V, int* order, BlockScratch& s
   if (n <= 1) {
     if (threadIdx.x == 0 && n == 1) order[0] = 0;
     __syncthreads();
-    return;
+    return 0;
   }
   // Skip a rotation when |a_pq| <= max(eps_r sqrt(|a_pp a_qq|), eps_a ||A||_F):
   // the relative test keeps the large eigenpairs accurate to working
@@ -215,8 +291,9 @@ __device__ void sym_eig(double* A, int n, double* V, int* order, BlockScratch& s
   double fro = 0.0;
   for (int j = warp; j < n; j += kWarps)
     for (int i = lane; i < n; i += 32) fro = fma(A[i + j * n], A[i + j * n], fro);
-  const double abs_thr = 1e-16 * sqrt(block_sum(fro, sc));
-  const double eps = 1e-15;
+  const double abs_thr = 1e-15 * sqrt(block_sum(fro, sc));
+  const double eps2 = 1e-28;  // relative test (1e-14)^2
+  int sweeps_done = 0;
   for (int sweep = 0; sweep < 20; ++sweep) {
     const int cur = sweep & 1;
     if (threadIdx.x == 0) sc.rotated[cur ^ 1] = 0;
@@ -239,14 +316,14 @@ __device__ void sym_eig(double* A, int n, double* V, int* order, BlockScratch& s
         if (q < n) {
           const double apq = A[p + q * n];
           const double app = A[p + p * n], aqq = A[q + q * n];
-          if (fabs(apq) > fmax(eps * sqrt(fabs(app)) * sqrt(fabs(aqq)), abs_thr)) {
-            const double tau = (aqq - app) / (2.0 * apq);
-            if (fabs(tau) > 1e150) {
-              t = 0.5 / tau;
-            } else {
-              t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-            }
-            c = 1.0 / sqrt(1.0 + t * t);
+          const double a2 = apq * apq;
+          if (a2 > eps2 * fabs(app * aqq) && fabs(apq) > abs_thr) {
+            // t = sign(tau) / (|tau| + sqrt(1 + tau^2)), tau = (aqq - app) / (2 apq),
+            // rewritten without the division by apq (GvL sym.schur2).
+            const double th = aqq - app, tw = 2.0 * apq;
+            const double den = fabs(th) + sqrt(fma(th, th, tw * tw));
+            t = (th >= 0.0 ? tw : -tw) / den;
+            c = rsqrt(fma(t, t, 1.0));
             s = t * c;
             sc.rotated[cur] = 1;
           }
@@ -308,6 +385,7 @@ __device__ void sym_eig(double* A, int n, double* V, int* order, BlockScratch& s
       }
       __syncthreads();
     }
+    ++sweeps_done;
     if (!sc.rotated[cur]) break;
     __syncthreads();
   }
@@ -322,6 +400,162 @@ __device__ void sym_eig(double* A, int n, double* V, int* order, BlockScratch& s
     order[rank] = i;
   }
   __syncthreads();
+  return sweeps_done;
+}
+
+// Shared-memory Jacobi for n <= 52 (pairs <= 26 fit one warp's lanes): every
+// warp recomputes the round's rotations in its lanes (lane k <-> pair k) and
+// exchanges them by shuffles, A is double-buffered (A0 -> A1) so a round is a
+// single barrier, and the round-robin pairing uses conditional subtraction.
+// S = dynamic shared base: A0 | A1 | V, each n*n doubles (col-major).
+constexpr int kFastEigN = 52;  // np <= 26 lanes; <= 4 pairs per warp needs >= 7 warps
+
+__device__ __forceinline__ void rr_pair(int r, int k, int n2, int& p, int& q) {
+  const int m = n2 - 1;
+  if (k == 0) {
+    p = r;
+    q = m;
+  } else {
+    p = r + k;
+    if (p >= m) p -= m;
+    q = r - k;
+    if (q < 0) q += m;
+  }
+  if (p > q) {
+    const int t = p;
+    p = q;
+    q = t;
+  }
+}
+
+__device__ int sym_eig_smem(double* S, int n, int* order, BlockScratch& sc) {
+  const int n2 = n + (n & 1);
+  const int np = n2 / 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* A = S;
+  double* B = S + n * n;
+  double* V = S + 2 * n * n;
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) V[idx] = (idx % (n + 1) == 0) ? 1.0 : 0.0;
+  double fro = 0.0;
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) fro = fma(A[idx], A[idx], fro);
+  const double abs_thr = 1e-15 * sqrt(block_sum(fro, sc));  // block_sum ends with a barrier
+  const double eps2 = 1e-28;
+  int sweeps_done = 0;
+  if (n <= 1) {
+    if (threadIdx.x == 0) order[0] = 0;
+    __syncthreads();
+    return 0;
+  }
+  const int nwarps = int(blockDim.x >> 5);
+  for (int sweep = 0; sweep < 20; ++sweep) {
+    int any = 0;
+    for (int r = 0; r < n2 - 1; ++r) {
+      // rotation of pair `lane` (identical in every warp)
+      int p = 0, q = 0;
+      double c = 1.0, sn = 0.0, t = 0.0;
+      if (lane < np) {
+        rr_pair(r, lane, n2, p, q);
+        if (q < n) {
+          const double apq = A[p + q * n];
+          const double app = A[p + p * n], aqq = A[q + q * n];
+          const double th = aqq - app, tw = 2.0 * apq;
+          const double h2 = fma(th, th, tw * tw);
+          const double den = fabs(th) + sqrt(h2);  // sqrt issued before the threshold test resolves
+          if (apq * apq > eps2 * fabs(app * aqq) && fabs(apq) > abs_thr) {
+            t = (th >= 0.0 ? tw : -tw) / den;
+            c = rsqrt(fma(t, t, 1.0));
+            sn = t * c;
+          }
+        }
+      }
+      any |= __any_sync(0xffffffffu, sn != 0.0);
+      // gather the pair parameters this warp needs up front (overlapped shuffles)
+      int p2v[4], q2v[4];
+      double c2v[4], s2v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int P2 = warp + u * nwarps;
+        const int src = P2 < 32 ? P2 : 0;
+        p2v[u] = __shfl_sync(0xffffffffu, p, src);
+        q2v[u] = __shfl_sync(0xffffffffu, q, src);
+        c2v[u] = __shfl_sync(0xffffffffu, c, src);
+        s2v[u] = __shfl_sync(0xffffffffu, sn, src);
+      }
+      // B = J^T A J, one owner per 2x2 block (warp <-> P2, lane <-> P1)
+      if (lane < np) {
+        const bool hq = q < n;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int P2 = warp + u * nwarps;
+          if (P2 >= np) break;
+          const int p2 = p2v[u], q2 = q2v[u];
+          const double c2 = c2v[u], s2 = s2v[u];
+          const bool hq2 = q2 < n;
+          if (lane == P2) {
+            const double app = A[p + p * n];
+            if (hq) {
+              const double apq = A[p + q * n], aqq = A[q + q * n];
+              B[p + p * n] = app - t * apq;
+              B[q + q * n] = aqq + t * apq;
+              B[p + q * n] = (sn != 0.0) ? 0.0 : apq;
+              B[q + p * n] = (sn != 0.0) ? 0.0 : apq;
+            } else {
+              B[p + p * n] = app;
+            }
+          } else {
+            const double m00 = A[p + p2 * n];
+            const double m01 = hq2 ? A[p + q2 * n] : 0.0;
+            const double m10 = hq ? A[q + p2 * n] : 0.0;
+            const double m11 = (hq && hq2) ? A[q + q2 * n] : 0.0;
+            const double x00 = c * m00 - sn * m10, x01 = c * m01 - sn * m11;
+            const double x10 = sn * m00 + c * m10, x11 = sn * m01 + c * m11;
+            B[p + p2 * n] = c2 * x00 - s2 * x01;
+            if (hq2) B[p + q2 * n] = s2 * x00 + c2 * x01;
+            if (hq) B[q + p2 * n] = c2 * x10 - s2 * x11;
+            if (hq && hq2) B[q + q2 * n] = s2 * x10 + c2 * x11;
+          }
+        }
+      }
+      // V = V J (warp <-> pair, lanes <-> rows); same pairs as the P2 set above
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int P1 = warp + u * nwarps;
+        if (P1 >= np) break;
+        const double s1 = s2v[u];
+        if (s1 == 0.0) continue;
+        const double c1 = c2v[u];
+        double* vp = V + p2v[u] * n;
+        double* vq = V + q2v[u] * n;
+        for (int i = lane; i < n; i += 32) {
+          const double a = vp[i], b = vq[i];
+          vp[i] = c1 * a - s1 * b;
+          vq[i] = s1 * a + c1 * b;
+        }
+      }
+      __syncthreads();
+      double* tmp = A;
+      A = B;
+      B = tmp;
+    }
+    ++sweeps_done;
+    if (!__syncthreads_or(any)) break;
+  }
+  // the diagonalised matrix must end in S[0 .. n*n)
+  if (A != S) {
+    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) S[idx] = A[idx];
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double li = S[i + i * n];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const double lj = S[j + j * n];
+      if (lj > li || (lj == li && j < i)) ++rank;
+    }
+    order[rank] = i;
+  }
+  __syncthreads();
+  return sweeps_done;
 }
 
 // Sign convention of linalg.cpp:15-31: each column's first max-|.| entry is

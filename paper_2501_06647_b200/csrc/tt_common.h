@@ -56,7 +56,7 @@ struct LeafDesc {
   double* out_f[kMaxP];            // output factor slots (ld = D_n; factor 0: ld = len)
   double* out_core;                // row-major core, capacity prod rc
   double* ws;                      // workspace (leaf_ws_size doubles)
-  int32_t* status;                 // [sweeps, converged, zero, pad, k_0..k_{p-1}] (4 + kMaxP)
+  int32_t* status;                 // [sweeps, converged, zero, deficient, k_0..k_7, eig calls, eig sweeps]
   double* objective;               // max_iters doubles
 };
 
@@ -91,7 +91,7 @@ struct Params {
   const double* stitch_init[kMaxP];  // stitch init factors U_m (m >= 1), D_m x rc_m
 };
 
-constexpr int kStatusInts = 4 + kMaxP;
+constexpr int kStatusInts = 4 + kMaxP + 10;  // ..., eig calls, Jacobi sweeps, kcycles per phase [8]
 
 // ---------------------------------------------------------------------------
 // Workspace layouts (in doubles). The misc tail holds reductions, sigma, order.

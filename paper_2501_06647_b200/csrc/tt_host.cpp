@@ -37,6 +37,8 @@ using Index = int64_t;
 namespace {
 
 thread_local std::string g_err;
+// problems, ALS sweeps, eig calls, Jacobi sweeps (cumulative, all trees)
+int64_t g_stats[12] = {};
 
 struct TTError : std::runtime_error {
   tt_status code;
@@ -232,7 +234,7 @@ struct Exec {
 
 // Result of one batched ALS problem after readback.
 struct ProblemStatus {
-  int sweeps = 0, converged = 0, zero = 0, deficient = 0;
+  int sweeps = 0, converged = 0, zero = 0, deficient = 0, eig_calls = 0, eig_sweeps = 0;
   Index k[kMaxP] = {};
   std::vector<double> objective;
 };
@@ -273,6 +275,13 @@ std::vector<ProblemStatus> run_leaf_batch(Exec& ex, const Params& prm, std::vect
     st[i].zero = s[2];
     st[i].deficient = s[3];
     for (int m = 0; m < kMaxP; ++m) st[i].k[m] = s[4 + m];
+    st[i].eig_calls = s[4 + kMaxP];
+    st[i].eig_sweeps = s[5 + kMaxP];
+    g_stats[0] += 1;
+    g_stats[1] += s[0];
+    g_stats[2] += s[4 + kMaxP];
+    g_stats[3] += s[5 + kMaxP];
+    for (int q = 0; q < 8; ++q) g_stats[4 + q] += s[6 + kMaxP + q];
     st[i].objective.assign(ho.begin() + size_t(i) * prm.max_iters, ho.begin() + size_t(i) * prm.max_iters + s[0]);
   }
   return st;
@@ -318,6 +327,13 @@ std::vector<ProblemStatus> run_stitch_batch(Exec& ex, const Params& prm, std::ve
     st[i].zero = s[2];
     st[i].deficient = s[3];
     for (int m = 0; m < kMaxP; ++m) st[i].k[m] = s[4 + m];
+    st[i].eig_calls = s[4 + kMaxP];
+    st[i].eig_sweeps = s[5 + kMaxP];
+    g_stats[0] += 1;
+    g_stats[1] += s[0];
+    g_stats[2] += s[4 + kMaxP];
+    g_stats[3] += s[5 + kMaxP];
+    for (int q = 0; q < 8; ++q) g_stats[4 + q] += s[6 + kMaxP + q];
     st[i].objective.assign(ho.begin() + size_t(i) * prm.max_iters, ho.begin() + size_t(i) * prm.max_iters + s[0]);
   }
   return st;
@@ -695,6 +711,9 @@ extern "C" {
 const char* tt_last_error(void) { return g_err.c_str(); }
 const char* tt_version(void) { return "tucktree_b200 0.1 (sm_100a)"; }
 int64_t tt_kernel_launches(void) { return launches(); }
+void tt_solver_stats(int64_t* out12) {
+  for (int i = 0; i < 12; ++i) out12[i] = g_stats[i];
+}
 
 tt_status tt_tree_create(const tt_config* cfg, tt_tree** out) {
   return guarded([&] {
@@ -704,8 +723,10 @@ tt_status tt_tree_create(const tt_config* cfg, tt_tree** out) {
     if (p < 2 || p > TT_MAX_ORDER) fail(TT_EINVAL, "StreamSegmentTree: order must be in [2, 8]");
     for (int m = 0; m < p - 1; ++m)
       if (cfg->nontemporal[m] < 1) fail(TT_EINVAL, "StreamSegmentTree: extents must be >= 1");
-    for (int m = 0; m < p; ++m)
+    for (int m = 0; m < p; ++m) {
       if (cfg->ranks[m] < 1) fail(TT_EINVAL, "StreamSegmentTree: ranks must be >= 1");
+      if (cfg->ranks[m] > 32) fail(TT_EINVAL, "StreamSegmentTree: ranks above 32 are not supported by this build");
+    }
     if (!(cfg->theta > 0.0 && cfg->theta < 1.0)) fail(TT_EINVAL, "StreamSegmentTree: theta must be in (0, 1)");
     if (cfg->max_iters < 1) fail(TT_EINVAL, "max_iters must be >= 1");
     if (cfg->tol <= 0.0) fail(TT_EINVAL, "tol must be > 0");
@@ -1252,6 +1273,7 @@ tt_status tt_tucker_als(const double* x, int32_t p, const int64_t* dims, const i
     for (int m = 0; m < p; ++m) {
       if (dims[m] < 1) fail(TT_EINVAL, "Shape: all dims must be >= 1");
       if (ranks[m] < 1) fail(TT_EINVAL, "clamp_ranks: ranks must be >= 1");
+      if (ranks[m] > 32) fail(TT_EINVAL, "tucker_als: ranks above 32 are not supported by this build");
     }
     StandaloneCtx& c = standalone(device);
     Exec& ex = *c.ex;
@@ -1319,8 +1341,12 @@ tt_status tt_stitch(int32_t nparts, int32_t p, const int64_t* part_dims, const i
     for (int i = 1; i < nparts; ++i)
       for (int m = 1; m < p; ++m)
         if (part_dims[i * p + m] != part_dims[m]) fail(TT_EINVAL, "stitch: non-temporal shape mismatch across parts");
-    for (int m = 0; m < p; ++m)
+    for (int m = 0; m < p; ++m) {
       if (ranks[m] < 1) fail(TT_EINVAL, "clamp_ranks: ranks must be >= 1");
+      if (ranks[m] > 32) fail(TT_EINVAL, "stitch: ranks above 32 are not supported by this build");
+    }
+    for (int i = 0; i < nparts * p; ++i)
+      if (part_ranks[i] > 32) fail(TT_EINVAL, "stitch: part ranks above 32 are not supported by this build");
     StandaloneCtx& c = standalone(device);
     Exec& ex = *c.ex;
     DeviceGuard g(device);

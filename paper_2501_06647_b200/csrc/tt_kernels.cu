@@ -43,11 +43,13 @@ __device__ __forceinline__ void ttm_elems(const double* __restrict__ in, int64_t
 // Dispatch: column-parallel when there are enough output columns.
 __device__ __forceinline__ void mode_product(const double* in, int64_t outer, int64_t d, int64_t inner,
                                              const double* M, int64_t ms_a, int64_t ms_j, int64_t r, double* out,
-                                             bool acc) {
+                                             bool acc, BlockScratch& sc, int slot = kPhTtm) {
+  const long long t0 = tstart();
   if (outer * inner >= 2 * int64_t(blockDim.x))
     ttm(in, outer, d, inner, M, ms_a, ms_j, r, out, acc);
   else
     ttm_elems(in, outer, d, inner, M, ms_a, ms_j, r, out, acc);
+  tstop(sc, slot, t0);
 }
 
 // A Gram eigenvalue carries an absolute rounding error ~eps * lambda_max, so
@@ -57,21 +59,44 @@ __device__ __forceinline__ bool gram_sigma_ok(double lam, double lam_max) {
   return lam > 1e-13 * lam_max && lam > 0.0;
 }
 
+__device__ __forceinline__ void tgemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t ars, int64_t acs,
+                                      const double* B, int64_t brs, int64_t bcs, double* C, int64_t crs, int64_t ccs,
+                                      bool acc, BlockScratch& sc) {
+  const long long t0 = tstart();
+  gemm(M, N, K, A, ars, acs, B, brs, bcs, C, crs, ccs, acc, sc);
+  tstop(sc, kPhGemm, t0);
+}
+
 // Runs the Jacobi solver on G (n x n), staging through shared memory when it
 // fits. Returns the pointer holding the eigenvectors; *diag receives the
 // pointer to the diagonalised matrix.
 __device__ double* eig_run(double* G, int n, double* V, int* order, double* dsm, double** diag, BlockScratch& sc) {
-  if (n <= kEigSmemN) {
+  int sw;
+  double* res;
+  const long long t0 = tstart();
+  if (n <= kFastEigN) {
+    bcopy(dsm, G, int64_t(n) * n);
+    sw = sym_eig_smem(dsm, n, order, sc);
+    *diag = dsm;
+    res = dsm + 2 * n * n;
+  } else if (n <= kEigSmemN) {
     double* As = dsm;
     double* Vs = dsm + n * n;
     bcopy(As, G, int64_t(n) * n);
-    sym_eig(As, n, Vs, order, sc);
+    sw = sym_eig(As, n, Vs, order, sc);
     *diag = As;
-    return Vs;
+    res = Vs;
+  } else {
+    sw = sym_eig(G, n, V, order, sc);
+    *diag = G;
+    res = V;
   }
-  sym_eig(G, n, V, order, sc);
-  *diag = G;
-  return V;
+  if (threadIdx.x == 0) {
+    sc.eig_calls += 1;
+    sc.eig_sweeps += sw;
+  }
+  tstop(sc, kPhEig, t0);
+  return res;
 }
 
 // leading_left_singular_vectors (linalg.cpp:45-64) of the mode unfolding of a
@@ -85,7 +110,9 @@ __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows, int64_
   double* diag = nullptr;
   if (rows <= cols) {
     const int n = int(rows);
+    long long tg = tstart();
     gram_rows(P, outer, rows, inner, G);
+    tstop(sc, kPhGram, tg);
     const double* Vp = eig_run(G, n, V, order, dsm, &diag, sc);
     for (int64_t idx = threadIdx.x; idx < rows * k; idx += blockDim.x) {
       const int64_t i = idx % rows, c = idx / rows;
@@ -94,7 +121,9 @@ __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows, int64_
     __syncthreads();
   } else {
     const int n = int(cols);
+    long long tg = tstart();
     gram_cols(P, outer, rows, inner, G);
+    tstop(sc, kPhGram, tg);
     const double* Vp = eig_run(G, n, V, order, dsm, &diag, sc);
     if (threadIdx.x < k) {
       const double l0 = fmax(diag[order[0] * (n + 1)], 0.0);
@@ -102,6 +131,7 @@ __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows, int64_
       sig[threadIdx.x] = gram_sigma_ok(lc, l0) ? 1.0 / sqrt(lc) : 0.0;
     }
     __syncthreads();
+    tg = tstart();
     for (int64_t idx = threadIdx.x; idx < rows * k; idx += blockDim.x) {
       const int64_t i = idx % rows, c = idx / rows;
       const double inv = sig[c];
@@ -117,15 +147,25 @@ __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows, int64_
       U[idx] = s * inv;
     }
     __syncthreads();
+    tstop(sc, kPhGram, tg);
+    const long long to = tstart();
     orthonormalize(U, rows, 0, int(k), rows, sc);
+    tstop(sc, kPhOrtho, to);
   }
+  const long long ts = tstart();
   sign_fix(U, rows, int(k), rows, nullptr, sc);
+  tstop(sc, kPhOrtho, ts);
 }
 
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads, 2) leaf_als_kernel(Params prm, const LeafDesc* __restrict__ descs) {
   __shared__ BlockScratch sc;
   extern __shared__ double dsm[];
+  const long long t_kernel = tstart();
+  if (threadIdx.x == 0) {
+    sc.eig_calls = sc.eig_sweeps = 0;
+    for (int i = 0; i < 8; ++i) sc.cyc[i] = 0;
+  }
   const LeafDesc D = descs[blockIdx.x];
   const int p = prm.p;
   int64_t d[kMaxP], rc[kMaxP], k[kMaxP];
@@ -162,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 2) leaf_als_kernel(Params prm, const
       for (int m = 1; m < p; ++m) {
         double* dst = B[tog];
         mode_product(src, prod_range(cur, 0, m), cur[m], prod_range(cur, m + 1, p), D.out_f[m], d[m], 1, k[m], dst,
-                     false);
+                     false, sc, m == 1 ? kPhBig : kPhTtm);
         cur[m] = k[m];
         src = dst;
         tog ^= 1;
@@ -170,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 2) leaf_als_kernel(Params prm, const
       llsv_unfold(src, 1, d[0], prod_range(cur, 1, p), k0n, D.out_f[0], G, V, misc, dsm, sc);
       k[0] = k0n;
       // ---- W = X x_0 U_0^T : (k0, D_1, ..., D_{p-1})
-      mode_product(X, 1, d[0], ns, D.out_f[0], d[0], 1, k[0], W, false);
+      mode_product(X, 1, d[0], ns, D.out_f[0], d[0], 1, k[0], W, false, sc, kPhBig);
       // ---- modes n >= 1 from W
       const double* Pn = W;
       int64_t pc[kMaxP];
@@ -184,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 2) leaf_als_kernel(Params prm, const
           if (m == n) continue;
           double* dst = B[t2];
           mode_product(s2, prod_range(pc, 0, m), pc[m], prod_range(pc, m + 1, p), D.out_f[m], d[m], 1, k[m], dst,
-                       false);
+                       false, sc);
           pc[m] = k[m];
           s2 = dst;
           t2 ^= 1;
@@ -195,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 2) leaf_als_kernel(Params prm, const
       }
       // ---- core = P_{p-1} x_{p-1} U_{p-1}^T  (== core_of(x, U), tucker.cpp:67-76)
       mode_product(Pn, prod_range(k, 0, p - 1), d[p - 1], 1, D.out_f[p - 1], d[p - 1], 1, k[p - 1], D.out_core,
-                   false);
+                   false, sc);
       const double core_sq = bsumsq(D.out_core, prod_range(k, 0, p), sc);
       const double res = fmax(0.0, norm_sq - core_sq);
       if (threadIdx.x == 0) D.objective[sweep] = res;
@@ -214,6 +254,10 @@ __global__ void __launch_bounds__(kThreads, 2) leaf_als_kernel(Params prm, const
     D.status[2] = norm_sq == 0.0;
     D.status[3] = 0;
     for (int m = 0; m < kMaxP; ++m) D.status[4 + m] = m < p ? int(k[m]) : 0;
+    D.status[4 + kMaxP] = sc.eig_calls;
+    D.status[5 + kMaxP] = sc.eig_sweeps;
+    sc.cyc[kPhAll] = clock64() - t_kernel;
+    for (int i = 0; i < 8; ++i) D.status[6 + kMaxP + i] = int(sc.cyc[i] >> 10);
   }
 }
 
@@ -246,7 +290,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     stitch_als_kernel(Params prm, const StitchDesc* __restrict__ descs, const StitchPart* __restrict__ parts_all) {
   __shared__ BlockScratch sc;
   __shared__ int flips[kMaxVec];
+  __shared__ int64_t idxbuf[kWarps * kMaxVec];
   extern __shared__ double dsm[];
+  const long long t_kernel = tstart();
+  if (threadIdx.x == 0) {
+    sc.eig_calls = sc.eig_sweeps = 0;
+    for (int i = 0; i < 8; ++i) sc.cyc[i] = 0;
+  }
   const StitchDesc D = descs[blockIdx.x];
   const StitchPart* parts = parts_all + D.part0;
   const int p = prm.p, s = D.nparts;
@@ -285,9 +335,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int64_t hk = prod_range(pv.rho, 1, p);
     if (pv.partial) {
       const double* vs = pv.v0 + pv.row0;
-      gemm(r0, r0, pv.len, vs, pv.ld0, 1, vs, 1, pv.ld0, Sp(i), 1, r0, false);
+      {
+        const long long tg = tstart();
+        gram_tall(vs, pv.ld0, pv.len, int(r0), Sp(i));
+        tstop(sc, kPhGram, tg);
+      }
       // ||H x_0 R||^2 = sum_ab S_ab (M0(H) M0(H)^T)_ab
-      gemm(r0, r0, hk, pv.core, hk, 1, pv.core, 1, hk, HH, 1, r0, false);
+      tgemm(r0, r0, hk, pv.core, hk, 1, pv.core, 1, hk, HH, 1, r0, false, sc);
       double acc = 0.0;
       for (int64_t e = threadIdx.x; e < r0 * r0; e += blockDim.x) acc = fma(Sp(i)[e], HH[e], acc);
       norm_sq += block_sum(acc, sc);
@@ -309,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int i = 0; i < s; ++i) {
       const PartView pv = load_part(parts[i]);
       for (int m = 1; m < p; ++m)
-        gemm(k[m], pv.rho[m], d[m], D.out_f[m], d[m], 1, pv.v[m], 1, d[m], Pm(i, m), 1, k[m], false);
+        tgemm(k[m], pv.rho[m], d[m], D.out_f[m], d[m], 1, pv.v[m], 1, d[m], Pm(i, m), 1, k[m], false, sc);
     }
     const double norm = sqrt(norm_sq);
     double prev_fit = nan("");
@@ -326,50 +380,91 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int m = p - 1; m >= 1; --m) {  // descending, as the reference
           double* dst = (m == 1) ? Cp(i) : T[tog];
           mode_product(src, prod_range(cur, 0, m), cur[m], prod_range(cur, m + 1, p), Pm(i, m), 1, k[m], k[m],
-                       dst, false);
+                       dst, false, sc);
           cur[m] = k[m];
           src = dst;
           tog ^= 1;
         }
       }
-      // G0 = Z0^T Z0 = sum_i C_i^T S_i C_i   (Q x Q)
+      // Row-compressed variant: with entire parts only, Z0 = blockdiag(V_i0) C
+      // (C = [C_1; ...; C_s], sum rho_i0 rows) and V_i0 orthonormal, so the left
+      // singular vectors of Z0 are blockdiag(V_i0) times the eigenvectors of
+      // C C^T — a (sum rho_i0)^2 problem instead of Q^2 when that is smaller
+      // (every two-part append stitch), with no Sigma^-1 amplification.
+      int64_t rsum = 0;
+      bool all_entire = true;
       for (int i = 0; i < s; ++i) {
-        const PartView pv = load_part(parts[i]);
-        const int64_t r0 = pv.rho[0];
-        const double* rhs = Cp(i);
-        if (pv.partial) {
-          gemm(r0, Q, r0, Sp(i), 1, r0, Cp(i), Q, 1, T[0], Q, 1, false);
-          rhs = T[0];
-        }
-        gemm(Q, Q, r0, Cp(i), 1, Q, rhs, Q, 1, G, 1, Q, i > 0);
+        rsum += parts[i].rho[0];
+        all_entire = all_entire && !parts[i].partial;
       }
-      {
+      if (all_entire && rsum < Q && k0n <= rsum) {  // else: rank-deficient Z0 needs the completion path
+        int64_t oi = 0;
+        for (int i = 0; i < s; ++i) {
+          const int64_t ri = parts[i].rho[0];
+          int64_t oj = 0;
+          for (int j = 0; j < s; ++j) {
+            const int64_t rj = parts[j].rho[0];
+            // H[oi.., oj..] = C_i C_j^T
+            tgemm(ri, rj, Q, Cp(i), Q, 1, Cp(j), 1, Q, G + oi + oj * rsum, 1, rsum, false, sc);
+            oj += rj;
+          }
+          oi += ri;
+        }
         int* order = reinterpret_cast<int*>(misc);
-        double* sig = misc + kMisc / 2;
         double* diag = nullptr;
-        if (threadIdx.x == 0) sc.ibcast[1] = 0;
-        const double* Vp = eig_run(G, int(Q), Vg, order, dsm, &diag, sc);
-        if (threadIdx.x < k0n) {
-          const double l0 = fmax(diag[order[0] * (Q + 1)], 0.0);
-          const double lc = fmax(diag[order[threadIdx.x] * (Q + 1)], 0.0);
-          const bool ok = gram_sigma_ok(lc, l0);
-          sig[threadIdx.x] = ok ? 1.0 / sqrt(lc) : 0.0;
-          if (!ok) atomicOr(&sc.ibcast[1], 1);
+        const double* Vp = eig_run(G, int(rsum), Vg, order, dsm, &diag, sc);
+        oi = 0;
+        for (int i = 0; i < s; ++i) {
+          const int64_t ri = parts[i].rho[0];
+          double* E = Ep(i);
+          for (int64_t idx = threadIdx.x; idx < ri * k0n; idx += blockDim.x) {
+            const int64_t a = idx % ri, c = idx / ri;
+            E[idx] = Vp[oi + a + int64_t(order[c]) * rsum];
+          }
+          oi += ri;
         }
         __syncthreads();
-        for (int64_t idx = threadIdx.x; idx < Q * k0n; idx += blockDim.x) {
-          const int64_t j = idx % Q, c = idx / Q;
-          wk[idx] = Vp[j + int64_t(order[c]) * Q] * sig[c];
+        any_zero_sigma = 0;
+      } else {
+        // G0 = Z0^T Z0 = sum_i C_i^T S_i C_i   (Q x Q)
+        for (int i = 0; i < s; ++i) {
+          const PartView pv = load_part(parts[i]);
+          const int64_t r0 = pv.rho[0];
+          const double* rhs = Cp(i);
+          if (pv.partial) {
+            tgemm(r0, Q, r0, Sp(i), 1, r0, Cp(i), Q, 1, T[0], Q, 1, false, sc);
+            rhs = T[0];
+          }
+          tgemm(Q, Q, r0, Cp(i), 1, Q, rhs, Q, 1, G, 1, Q, i > 0, sc);
         }
-        __syncthreads();
-        any_zero_sigma = sc.ibcast[1];
-      }
-      // E_i = C_i W Sigma^-1 (rho0 x k0);  A_i = S_i E_i = (U0[rows_i]^T V_i0)^T
-      for (int i = 0; i < s; ++i) {
-        const PartView pv = load_part(parts[i]);
-        const int64_t r0 = pv.rho[0];
-        gemm(r0, k0n, Q, Cp(i), Q, 1, wk, 1, Q, Ep(i), 1, r0, false);
-        if (pv.partial) gemm(r0, k0n, r0, Sp(i), 1, r0, Ep(i), 1, r0, Ap(i), 1, r0, false);
+        {
+          int* order = reinterpret_cast<int*>(misc);
+          double* sig = misc + kMisc / 2;
+          double* diag = nullptr;
+          if (threadIdx.x == 0) sc.ibcast[1] = 0;
+          const double* Vp = eig_run(G, int(Q), Vg, order, dsm, &diag, sc);
+          if (threadIdx.x < k0n) {
+            const double l0 = fmax(diag[order[0] * (Q + 1)], 0.0);
+            const double lc = fmax(diag[order[threadIdx.x] * (Q + 1)], 0.0);
+            const bool ok = gram_sigma_ok(lc, l0);
+            sig[threadIdx.x] = ok ? 1.0 / sqrt(lc) : 0.0;
+            if (!ok) atomicOr(&sc.ibcast[1], 1);
+          }
+          __syncthreads();
+          for (int64_t idx = threadIdx.x; idx < Q * k0n; idx += blockDim.x) {
+            const int64_t j = idx % Q, c = idx / Q;
+            wk[idx] = Vp[j + int64_t(order[c]) * Q] * sig[c];
+          }
+          __syncthreads();
+          any_zero_sigma = sc.ibcast[1];
+        }
+        // E_i = C_i W Sigma^-1 (rho0 x k0);  A_i = S_i E_i = (U0[rows_i]^T V_i0)^T
+        for (int i = 0; i < s; ++i) {
+          const PartView pv = load_part(parts[i]);
+          const int64_t r0 = pv.rho[0];
+          tgemm(r0, k0n, Q, Cp(i), Q, 1, wk, 1, Q, Ep(i), 1, r0, false, sc);
+          if (pv.partial) tgemm(r0, k0n, r0, Sp(i), 1, r0, Ep(i), 1, r0, Ap(i), 1, r0, false, sc);
+        }
       }
       k[0] = k0n;
       // ================= modes n >= 1 (stitch_nontemporal_unfolding, stitch.cpp:75-108)
@@ -384,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           for (int m = 0; m < p; ++m) cur[m] = pv.rho[m];
           const double* A0 = pv.partial ? Ap(i) : Ep(i);
           // x_0 (U0[rows_i]^T V_i0): M(a, j) = A0[j + a*rho0]
-          mode_product(pv.core, 1, cur[0], prod_range(cur, 1, p), A0, cur[0], 1, k[0], T[0], false);
+          mode_product(pv.core, 1, cur[0], prod_range(cur, 1, p), A0, cur[0], 1, k[0], T[0], false, sc);
           cur[0] = k[0];
           const double* src = T[0];
           int tog = 1;
@@ -392,24 +487,24 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (m == n) continue;
             double* dst = T[tog];
             mode_product(src, prod_range(cur, 0, m), cur[m], prod_range(cur, m + 1, p), Pm(i, m), 1, k[m], k[m],
-                         dst, false);
+                         dst, false, sc);
             cur[m] = k[m];
             src = dst;
             tog ^= 1;
           }
           // Z_n += F x_n V_in
-          mode_product(src, zo, cur[n], zi, pv.v[n], 1, d[n], d[n], Z, i > 0);
+          mode_product(src, zo, cur[n], zi, pv.v[n], 1, d[n], d[n], Z, i > 0, sc);
         }
         llsv_unfold(Z, zo, d[n], zi, kn, D.out_f[n], G, Vg, misc, dsm, sc);
         k[n] = kn;
         for (int i = 0; i < s; ++i) {
           const PartView pv = load_part(parts[i]);
-          gemm(k[n], pv.rho[n], d[n], D.out_f[n], d[n], 1, pv.v[n], 1, d[n], Pm(i, n), 1, k[n], false);
+          tgemm(k[n], pv.rho[n], d[n], D.out_f[n], d[n], 1, pv.v[n], 1, d[n], Pm(i, n), 1, k[n], false, sc);
         }
       }
       // ================= core: fold Z_{p-1} and project the last mode (stitch.cpp:163-172)
       mode_product(Z, prod_range(k, 0, p - 1), d[p - 1], 1, D.out_f[p - 1], d[p - 1], 1, k[p - 1], D.out_core,
-                   false);
+                   false, sc);
       const double core_sq = bsumsq(D.out_core, prod_range(k, 0, p), sc);
       const double res = fmax(0.0, norm_sq - core_sq);
       if (threadIdx.x == 0) D.objective[sweep] = res;
@@ -424,30 +519,98 @@ __global__ void __launch_bounds__(kThreads, 2)
     // ================= materialise U_0 = blockdiag(Vsub_i) [E_i] (L x k0), sign-fixed
     const int64_t k0 = k[0];
     double* U0 = D.out_f[0];
-    {
+    const long long tu = tstart();
+    // Row-parallel materialisation in column chunks of KU: each thread owns
+    // rows, keeps the first max-|.| row per column (sign convention), then a
+    // block argmax picks each column's sign. Rows of part i: Vsub_i[r,:] E_i.
+    constexpr int KU = 8;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    for (int c0 = 0; c0 < k0; c0 += KU) {
+      const int nc = int(imin(KU, k0 - c0));
+      double best[KU];
+      int64_t bidx[KU];
+#pragma unroll
+      for (int c = 0; c < KU; ++c) {
+        best[c] = -1.0;
+        bidx[c] = 0;
+      }
       int64_t off = 0;
       for (int i = 0; i < s; ++i) {
         const PartView pv = load_part(parts[i]);
         const int64_t r0 = pv.rho[0];
         const double* vs = pv.v0 + pv.row0;
-        const double* E = Ep(i);
-        const int64_t tot = pv.len * k0;
-        for (int64_t idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-          const int64_t r = idx % pv.len, c = idx / pv.len;
-          double acc = 0.0;
-          for (int64_t a = 0; a < r0; ++a) acc = fma(vs[r + a * pv.ld0], E[a + c * r0], acc);
-          U0[off + r + c * D.L] = acc;
+        const double* E = Ep(i) + c0 * r0;
+        for (int64_t r = threadIdx.x; r < pv.len; r += blockDim.x) {
+          double out[KU];
+#pragma unroll
+          for (int c = 0; c < KU; ++c) out[c] = 0.0;
+          for (int64_t a = 0; a < r0; ++a) {
+            const double v = vs[r + a * pv.ld0];
+#pragma unroll
+            for (int c = 0; c < KU; ++c)
+              if (c < nc) out[c] = fma(v, E[a + c * r0], out[c]);
+          }
+#pragma unroll
+          for (int c = 0; c < KU; ++c)
+            if (c < nc) {
+              U0[off + r + (c0 + c) * D.L] = out[c];
+              const double m = fabs(out[c]);
+              if (m > best[c]) {
+                best[c] = m;
+                bidx[c] = off + r;
+              }
+            }
         }
         off += pv.len;
       }
+#pragma unroll
+      for (int c = 0; c < KU; ++c) {
+        double b = best[c];
+        int64_t bi = bidx[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, b, o);
+          const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > b || (ob == b && oi < bi)) {
+            b = ob;
+            bi = oi;
+          }
+        }
+        if (l == 0 && c < nc) {
+          sc.red[w * kMaxVec + c0 + c] = b;
+          idxbuf[w * kMaxVec + c0 + c] = bi;
+        }
+      }
+    }
+    __syncthreads();
+    if (any_zero_sigma) {
+      orthonormalize(U0, D.L, 0, int(k0), D.L, sc);
+      sign_fix(U0, D.L, int(k0), D.L, flips, sc);
+    } else {
+      if (threadIdx.x < k0) {
+        const int c = threadIdx.x;
+        double b = sc.red[c];
+        int64_t bi = idxbuf[c];
+        for (int ww = 1; ww < kWarps; ++ww) {
+          const double ob = sc.red[ww * kMaxVec + c];
+          const int64_t oi = idxbuf[ww * kMaxVec + c];
+          if (ob > b || (ob == b && oi < bi)) {
+            b = ob;
+            bi = oi;
+          }
+        }
+        flips[c] = U0[bi + c * D.L] < 0.0;
+      }
+      __syncthreads();
+      for (int64_t idx = threadIdx.x; idx < D.L * k0; idx += blockDim.x)
+        if (flips[idx / D.L]) U0[idx] = -U0[idx];
       __syncthreads();
     }
-    if (any_zero_sigma) orthonormalize(U0, D.L, 0, int(k0), D.L, sc);
-    sign_fix(U0, D.L, int(k0), D.L, flips, sc);
     const int64_t slice = prod_range(k, 1, p);
     for (int64_t e = threadIdx.x; e < k0 * slice; e += blockDim.x)
       if (flips[e / slice]) D.out_core[e] = -D.out_core[e];
     __syncthreads();
+    tstop(sc, kPhU0, tu);
   }
   if (threadIdx.x == 0) {
     D.status[0] = sweeps;
@@ -455,6 +618,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     D.status[2] = norm_sq == 0.0;
     D.status[3] = any_zero_sigma;
     for (int m = 0; m < kMaxP; ++m) D.status[4 + m] = m < p ? int(k[m]) : 0;
+    D.status[4 + kMaxP] = sc.eig_calls;
+    D.status[5 + kMaxP] = sc.eig_sweeps;
+    sc.cyc[kPhAll] = clock64() - t_kernel;
+    for (int i = 0; i < 8; ++i) D.status[6 + kMaxP + i] = int(sc.cyc[i] >> 10);
   }
 }
 

@@ -62,6 +62,7 @@ SIGNATURES = {
     "tt_last_error": (C.c_char_p, []),
     "tt_version": (C.c_char_p, []),
     "tt_kernel_launches": (i64, []),
+    "tt_solver_stats": (None, [i64ptr]),
     "tt_tree_create": (C.c_int, [C.POINTER(TTConfig), C.POINTER(vp)]),
     "tt_tree_destroy": (None, [vp]),
     "tt_tree_clear": (C.c_int, [vp]),
@@ -434,3 +435,11 @@ class StreamSegmentTree:
 
 def kernel_launches() -> int:
     return lib().tt_kernel_launches()
+
+
+def solver_stats() -> dict:
+    """Cumulative ALS/eigensolver counters (problems, ALS sweeps, eig calls, Jacobi sweeps)."""
+    out = np.zeros(12, dtype=np.int64)
+    lib().tt_solver_stats(out.ctypes.data_as(i64ptr))
+    return dict(zip(("problems", "als_sweeps", "eig_calls", "jacobi_sweeps", "kcyc_eig", "kcyc_gram", "kcyc_ttm",
+                     "kcyc_gemm", "kcyc_ortho_sign", "kcyc_u0", "kcyc_leaf_x", "kcyc_problem"), (int(v) for v in out)))
