@@ -34,10 +34,15 @@ struct BlockScratch {
 
 // Phase-timer slots (thread 0 accumulates clock64 deltas; instrumentation).
 enum { kPhEig = 0, kPhGram = 1, kPhTtm = 2, kPhGemm = 3, kPhOrtho = 4, kPhU0 = 5, kPhBig = 6, kPhAll = 7 };
+#ifdef TT_INSTRUMENT
 __device__ __forceinline__ long long tstart() { return threadIdx.x == 0 ? clock64() : 0; }
 __device__ __forceinline__ void tstop(BlockScratch& sc, int slot, long long t0) {
   if (threadIdx.x == 0) sc.cyc[slot] += clock64() - t0;
 }
+#else
+__device__ __forceinline__ long long tstart() { return 0; }
+__device__ __forceinline__ void tstop(BlockScratch&, int, long long) {}
+#endif
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

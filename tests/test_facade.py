@@ -1,0 +1,32 @@
+"""The header-only C++ facade (include/tucktree_b200.hpp) compiles with g++
+against the engine library and reproduces the reference KATs through it."""
+import os
+import subprocess
+
+import pytest
+
+from paper_2501_06647_b200 import build as B
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _compile(tmp_path):
+    lib = B.build()
+    exe = str(tmp_path / "facade_check")
+    subprocess.check_call(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "tests", "cpp", "facade_check.cpp"), lib,
+                           "-Wl,-rpath," + os.path.dirname(lib), "-o", exe])
+    return exe
+
+
+def test_facade_structure(tmp_path):
+    exe = _compile(tmp_path)
+    r = subprocess.run([exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_facade_gpu(tmp_path):
+    exe = _compile(tmp_path)
+    r = subprocess.run([exe, "gpu"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
