@@ -210,8 +210,9 @@ int64_t tt_kernel_launches(void);
  * [0] ALS problems, [1] ALS sweeps, [2] eigen-solves, [3] Jacobi sweeps,
  * [4..11] thousands of SM cycles summed over problems in: eigen-solves, Gram
  * matrices (+U assembly), small mode products, small GEMMs, orthonormalise +
- * sign fix, U_0 materialisation, leaf X passes, whole problem.            */
-void tt_solver_stats(int64_t* out12);
+ * sign fix, U_0 materialisation, leaf X passes, whole problem; [12..13]
+ * subspace-iteration solves that converged / fell back to Jacobi.         */
+void tt_solver_stats(int64_t* out14);
 
 #ifdef __cplusplus
 }

@@ -29,6 +29,7 @@ struct BlockScratch {
   int jp[256], jq[256];
   int rotated[2];
   int eig_calls, eig_sweeps;  // instrumentation (Jacobi sweeps per problem)
+  int si_ok, si_fail;         // subspace-iteration outcomes
   long long cyc[8];           // instrumentation: cycles per phase (see kPhase*)
 };
 

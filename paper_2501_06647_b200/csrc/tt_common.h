@@ -91,15 +91,21 @@ struct Params {
   const double* stitch_init[kMaxP];  // stitch init factors U_m (m >= 1), D_m x rc_m
 };
 
-constexpr int kStatusInts = 4 + kMaxP + 10;  // ..., eig calls, Jacobi sweeps, kcycles per phase [8]
+constexpr int kStatusInts = 4 + kMaxP + 12;  // ..., eig calls, Jacobi sweeps, kcycles[8], subspace ok/fail
 
 // ---------------------------------------------------------------------------
 // Workspace layouts (in doubles). The misc tail holds reductions, sigma, order.
 constexpr int64_t kMisc = 2048;
 
 struct LeafWs {
-  int64_t W, B1, B2, G, V, misc, total, gram_n;
+  int64_t W, B1, B2, G, V, SI, misc, total, gram_n;
 };
+
+// Subspace-iteration scratch: U/W (rows x k), Y (cols x k), small k x k
+// matrices and the unfolding column-offset table.
+TT_HD int64_t si_size(int64_t max_rows, int64_t max_cols, int64_t kmax) {
+  return 2 * max_rows * kmax + max_cols * kmax + 8 * kmax * kmax + max_cols + 64;
+}
 
 TT_HD LeafWs leaf_ws_layout(int p, int64_t len, const int64_t* d, const int64_t* req) {
   int64_t dd[kMaxP], rc[kMaxP];
@@ -119,14 +125,20 @@ TT_HD LeafWs leaf_ws_layout(int p, int64_t len, const int64_t* d, const int64_t*
   w.B2 = w.B1 + sB;
   w.G = w.B2 + sB;
   w.V = w.G + g * g;
-  w.misc = w.V + g * g;
+  int64_t maxrows = len, kmax = 1;
+  for (int m = 0; m < p; ++m) {
+    maxrows = imax(maxrows, dd[m]);
+    kmax = imax(kmax, rc[m]);
+  }
+  w.SI = w.V + g * g;
+  w.misc = w.SI + si_size(maxrows, g, kmax);
   w.total = w.misc + kMisc + 4 * g;
   w.total = (w.total + 31) & ~int64_t(31);
   return w;
 }
 
 struct StitchWs {
-  int64_t P, C, S, E, A, G, V, T1, T2, Z, WK, HH, misc, total, gram_n;
+  int64_t P, C, S, E, A, G, V, T1, T2, Z, WK, HH, SI, misc, total, gram_n;
   int64_t per_part_P, per_part_C, per_part_S, per_part_E;
 };
 
@@ -164,7 +176,11 @@ TT_HD StitchWs stitch_ws_layout(int p, int64_t L, const int64_t* d, const int64_
   w.Z = w.T2 + chain;
   w.WK = w.Z + z;
   w.HH = w.WK + g * rc[0];
-  w.misc = w.HH + rcx[0] * rcx[0];
+  int64_t maxrows = 1, kmax = 1;
+  for (int m = 1; m < p; ++m) maxrows = imax(maxrows, dd[m]);
+  for (int m = 0; m < p; ++m) kmax = imax(kmax, rc[m]);
+  w.SI = w.HH + rcx[0] * rcx[0];
+  w.misc = w.SI + si_size(maxrows, g, kmax);
   w.total = w.misc + kMisc + 4 * g;
   w.total = (w.total + 31) & ~int64_t(31);
   return w;

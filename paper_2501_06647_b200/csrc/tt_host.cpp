@@ -38,7 +38,7 @@ namespace {
 
 thread_local std::string g_err;
 // problems, ALS sweeps, eig calls, Jacobi sweeps (cumulative, all trees)
-int64_t g_stats[12] = {};
+int64_t g_stats[14] = {};
 
 struct TTError : std::runtime_error {
   tt_status code;
@@ -282,6 +282,8 @@ std::vector<ProblemStatus> run_leaf_batch(Exec& ex, const Params& prm, std::vect
     g_stats[2] += s[4 + kMaxP];
     g_stats[3] += s[5 + kMaxP];
     for (int q = 0; q < 8; ++q) g_stats[4 + q] += s[6 + kMaxP + q];
+    g_stats[12] += s[14 + kMaxP];
+    g_stats[13] += s[15 + kMaxP];
     st[i].objective.assign(ho.begin() + size_t(i) * prm.max_iters, ho.begin() + size_t(i) * prm.max_iters + s[0]);
   }
   return st;
@@ -334,6 +336,8 @@ std::vector<ProblemStatus> run_stitch_batch(Exec& ex, const Params& prm, std::ve
     g_stats[2] += s[4 + kMaxP];
     g_stats[3] += s[5 + kMaxP];
     for (int q = 0; q < 8; ++q) g_stats[4 + q] += s[6 + kMaxP + q];
+    g_stats[12] += s[14 + kMaxP];
+    g_stats[13] += s[15 + kMaxP];
     st[i].objective.assign(ho.begin() + size_t(i) * prm.max_iters, ho.begin() + size_t(i) * prm.max_iters + s[0]);
   }
   return st;
@@ -711,8 +715,8 @@ extern "C" {
 const char* tt_last_error(void) { return g_err.c_str(); }
 const char* tt_version(void) { return "tucktree_b200 0.1 (sm_100a)"; }
 int64_t tt_kernel_launches(void) { return launches(); }
-void tt_solver_stats(int64_t* out12) {
-  for (int i = 0; i < 12; ++i) out12[i] = g_stats[i];
+void tt_solver_stats(int64_t* out14) {
+  for (int i = 0; i < 14; ++i) out14[i] = g_stats[i];
 }
 
 tt_status tt_tree_create(const tt_config* cfg, tt_tree** out) {

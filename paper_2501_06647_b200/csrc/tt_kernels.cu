@@ -99,12 +99,236 @@ __device__ double* eig_run(double* G, int n, double* V, int* order, double* dsm,
   return res;
 }
 
+// ---------------------------------------------------------------------------
+// Block subspace iteration for the top-k left singular subspace of a tall
+// unfolding A (rows x cols, cols >= 2k), warm-started from the factor's current
+// value. Each iteration: Y = A^T U, B = Y^T Y (= U^T A A^T U), W = A Y; stop
+// when ||W - U B||_F <= 1e-13 ||B||_F (the subspace is then accurate to
+// ~1e-13 lambda_1 / gap); otherwise U = orth(W) by CholeskyQR2. A Rayleigh-Ritz
+// rotation by the eigenvectors of B then gives the exact top-k singular
+// vectors, identical (to rounding) to the SVD route of the reference. Returns
+// false — the caller falls back to Gram + Jacobi — when it does not converge in
+// kSiMaxIter iterations or CholeskyQR breaks down (rank deficiency, tiny gap).
+constexpr int kSiMaxIter = 40;
+constexpr int kSiMaxK = 16;     // register-tile bound on k
+constexpr int kSiMaxYK = 512;   // bound on cols * k (16 outputs per lane)
+
+// Warp 0 factors the SPD k x k matrix G = L L^T and writes Linv = L^{-1}
+// (both col-major, lower). Sets sc.ibcast[2] = 1 on a failed pivot.
+__device__ void chol_inv_warp(const double* G, int k, double* L, double* Linv, BlockScratch& sc) {
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  double dmax = 0.0;
+  for (int j = 0; j < k; ++j) dmax = fmax(dmax, G[j + j * k]);
+  bool ok = dmax > 0.0;
+  for (int j = 0; j < k && ok; ++j) {
+    double sdiag = 0.0;
+    if (lane == j) {
+      sdiag = G[j + j * k];
+      for (int l = 0; l < j; ++l) sdiag -= L[j + l * k] * L[j + l * k];
+    }
+    sdiag = __shfl_sync(0xffffffffu, sdiag, j);
+    if (!(sdiag > 1e-26 * dmax)) {
+      ok = false;
+      break;
+    }
+    const double ljj = sqrt(sdiag), inv = 1.0 / ljj;
+    if (lane > j && lane < k) {
+      double v = G[lane + j * k];
+      for (int l = 0; l < j; ++l) v -= L[lane + l * k] * L[j + l * k];
+      L[lane + j * k] = v * inv;
+    }
+    if (lane == j) L[j + j * k] = ljj;
+    __syncwarp();
+  }
+  if (!ok) {
+    if (lane == 0) sc.ibcast[2] = 1;
+    return;
+  }
+  if (lane < k) {  // column `lane` of L^{-1} by forward substitution
+    const int c = lane;
+    for (int i = 0; i < c; ++i) Linv[i + c * k] = 0.0;
+    for (int i = c; i < k; ++i) {
+      double v = (i == c) ? 1.0 : 0.0;
+      for (int l = c; l < i; ++l) v -= L[i + l * k] * Linv[l + c * k];
+      Linv[i + c * k] = v / L[i + i * k];
+    }
+  }
+}
+
+// W (rows x k, ld rows) <- W L^{-T}, where W^T W = L L^T (one CholeskyQR pass).
+__device__ bool cholqr_pass(double* W, int64_t rows, int k, double* small, BlockScratch& sc) {
+  double* G = small;
+  double* L = small + k * k;
+  double* Li = small + 2 * k * k;
+  gram_tall(W, rows, rows, k, G);
+  if (threadIdx.x == 0) sc.ibcast[2] = 0;
+  __syncthreads();
+  chol_inv_warp(G, k, L, Li, sc);
+  __syncthreads();
+  if (sc.ibcast[2]) return false;
+  for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) {
+    double w[kSiMaxK];
+#pragma unroll
+    for (int l = 0; l < kSiMaxK; ++l) w[l] = l < k ? W[r + l * rows] : 0.0;
+#pragma unroll
+    for (int j = 0; j < kSiMaxK; ++j) {
+      if (j >= k) break;
+      double v = 0.0;
+#pragma unroll
+      for (int l = 0; l < kSiMaxK; ++l)
+        if (l <= j) v = fma(w[l], Li[j + l * k], v);
+      W[r + j * rows] = v;
+    }
+  }
+  __syncthreads();
+  return true;
+}
+
+// Y (cols x k) = A^T U with A(i, c) = P[offc[c] + i*inner]; split over warps by
+// row chunks, partial sums reduced through shared memory (cols*k <= 1024).
+__device__ void unfold_At_U(const double* __restrict__ P, const int* __restrict__ offc, int64_t rows, int64_t inner,
+                            int cols, const double* __restrict__ U, int k, double* __restrict__ Y, double* part,
+                            BlockScratch& sc) {
+  constexpr int OPL = kSiMaxYK / 32;  // outputs per lane
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = int(blockDim.x >> 5);
+  const int ne = cols * k;
+  const int64_t chunk = (rows + nw - 1) / nw;
+  const int64_t i0 = warp * chunk, i1 = imin(rows, i0 + chunk);
+  double acc[OPL];
+  int oc[OPL], oj[OPL];
+#pragma unroll
+  for (int u = 0; u < OPL; ++u) {
+    const int e = lane + 32 * u;
+    const int c = e < ne ? e % cols : 0;
+    oc[u] = offc[c];
+    oj[u] = e < ne ? e / cols : 0;
+    acc[u] = 0.0;
+  }
+  for (int64_t i = i0; i < i1; ++i) {
+    const double* Pi = P + i * inner;
+    const double* Ui = U + i;
+#pragma unroll
+    for (int u = 0; u < OPL; ++u)
+      if (lane + 32 * u < ne) acc[u] = fma(Pi[oc[u]], Ui[int64_t(oj[u]) * rows], acc[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < OPL; ++u)
+    if (lane + 32 * u < ne) part[warp * ne + lane + 32 * u] = acc[u];
+  __syncthreads();
+  for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+    double v = 0.0;
+    for (int w = 0; w < nw; ++w) v += part[w * ne + e];
+    Y[(e % cols) + int64_t(e / cols) * cols] = v;
+  }
+  __syncthreads();
+}
+
+__device__ bool llsv_subspace(const double* P, int64_t outer, int64_t rows, int64_t inner, int k, int kprev, double* U,
+                              double* si, double* dsm, double* misc, BlockScratch& sc) {
+  const int cols = int(outer * inner);
+  double* W = si;                          // rows x k
+  double* Y = W + rows * k;                // cols x k
+  double* small = Y + int64_t(cols) * k;   // 4 k x k
+  double* B = small + 4 * k * k;           // k x k
+  int* offc = reinterpret_cast<int*>(B + k * k);
+  for (int c = threadIdx.x; c < cols; c += blockDim.x)
+    offc[c] = int((c / inner) * rows * inner + (c % inner));
+  // warm start: the current factor's columns, padded with canonical vectors
+  if (kprev < k) {
+    for (int64_t idx = threadIdx.x; idx < rows * (k - kprev); idx += blockDim.x) {
+      const int64_t r = idx % rows, c = kprev + idx / rows;
+      U[r + c * rows] = (r == (c * 7919) % rows) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    if (!cholqr_pass(U, rows, k, small, sc) || !cholqr_pass(U, rows, k, small, sc)) return false;
+  } else {
+    __syncthreads();
+  }
+  bool conv = false;
+  for (int it = 0; it < kSiMaxIter; ++it) {
+    unfold_At_U(P, offc, rows, inner, cols, U, k, Y, dsm, sc);
+    gram_tall(Y, cols, cols, k, B);
+    // W = A Y (row-parallel, k outputs per row)
+    for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+      double acc[kSiMaxK];
+#pragma unroll
+      for (int j = 0; j < kSiMaxK; ++j) acc[j] = 0.0;
+      const double* Pi = P + i * inner;
+      for (int c = 0; c < cols; ++c) {
+        const double a = Pi[offc[c]];
+#pragma unroll
+        for (int j = 0; j < kSiMaxK; ++j)
+          if (j < k) acc[j] = fma(a, Y[c + j * cols], acc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < kSiMaxK; ++j)
+        if (j < k) W[i + j * rows] = acc[j];
+    }
+    __syncthreads();
+    double rsq = 0.0, bsq = 0.0;
+    for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+      for (int j = 0; j < k; ++j) {
+        double v = W[i + j * rows];
+        for (int l = 0; l < k; ++l) v = fma(-U[i + l * rows], B[l + j * k], v);
+        rsq = fma(v, v, rsq);
+      }
+    }
+    for (int e = threadIdx.x; e < k * k; e += blockDim.x) bsq = fma(B[e], B[e], bsq);
+    rsq = block_sum(rsq, sc);
+    bsq = block_sum(bsq, sc);
+    if (bsq > 0.0 && rsq <= 1e-26 * bsq) {
+      conv = true;
+      break;
+    }
+    if (!(bsq > 0.0)) return false;
+    if (!cholqr_pass(W, rows, k, small, sc) || !cholqr_pass(W, rows, k, small, sc)) return false;
+    for (int64_t idx = threadIdx.x; idx < rows * k; idx += blockDim.x) U[idx] = W[idx];
+    __syncthreads();
+  }
+  if (!conv) return false;
+  // Rayleigh-Ritz: U <- U R with B R = R diag(lambda), descending
+  int* order = reinterpret_cast<int*>(misc);
+  double* diag = nullptr;
+  const double* R = eig_run(B, k, small, order, dsm, &diag, sc);
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+    double u[kSiMaxK];
+#pragma unroll
+    for (int l = 0; l < kSiMaxK; ++l) u[l] = l < k ? U[i + l * rows] : 0.0;
+    for (int j = 0; j < k; ++j) {
+      const double* rj = R + int64_t(order[j]) * k;
+      double v = 0.0;
+#pragma unroll
+      for (int l = 0; l < kSiMaxK; ++l)
+        if (l < k) v = fma(u[l], rj[l], v);
+      W[i + j * rows] = v;
+    }
+  }
+  __syncthreads();
+  for (int64_t idx = threadIdx.x; idx < rows * k; idx += blockDim.x) U[idx] = W[idx];
+  __syncthreads();
+  sign_fix(U, rows, k, rows, nullptr, sc);
+  return true;
+}
+
 // leading_left_singular_vectors (linalg.cpp:45-64) of the mode unfolding of a
 // row-major (outer, rows, inner) tensor, through the Gram matrix of its
 // smaller side. U: rows x k (ld rows), sign-fixed.
 __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows, int64_t inner, int64_t k, double* U,
-                            double* G, double* V, double* misc, double* dsm, BlockScratch& sc) {
+                            double* G, double* V, double* misc, double* dsm, BlockScratch& sc, int64_t kprev = 0,
+                            double* si = nullptr) {
   const int64_t cols = outer * inner;
+  if (si != nullptr && kprev > 0 && rows > cols && cols >= 2 * k && cols * k <= kSiMaxYK && k <= kSiMaxK) {
+    const long long t0 = tstart();
+    const bool ok = llsv_subspace(P, outer, rows, inner, int(k), int(imin(kprev, k)), U, si, dsm, misc, sc);
+    tstop(sc, kPhEig, t0);
+    if (ok) {
+      if (threadIdx.x == 0) sc.si_ok += 1;
+      return;
+    }
+    if (threadIdx.x == 0) sc.si_fail += 1;
+  }
   int* order = reinterpret_cast<int*>(misc);
   double* sig = misc + kMisc / 2;
   double* diag = nullptr;
@@ -163,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 2) leaf_als_kernel(Params prm, const
   extern __shared__ double dsm[];
   const long long t_kernel = tstart();
   if (threadIdx.x == 0) {
-    sc.eig_calls = sc.eig_sweeps = 0;
+    sc.eig_calls = sc.eig_sweeps = sc.si_ok = sc.si_fail = 0;
     for (int i = 0; i < 8; ++i) sc.cyc[i] = 0;
   }
   const LeafDesc D = descs[blockIdx.x];
@@ -207,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 2) leaf_als_kernel(Params prm, const
         src = dst;
         tog ^= 1;
       }
-      llsv_unfold(src, 1, d[0], prod_range(cur, 1, p), k0n, D.out_f[0], G, V, misc, dsm, sc);
+      llsv_unfold(src, 1, d[0], prod_range(cur, 1, p), k0n, D.out_f[0], G, V, misc, dsm, sc, k[0], D.ws + lay.SI);
       k[0] = k0n;
       // ---- W = X x_0 U_0^T : (k0, D_1, ..., D_{p-1})
       mode_product(X, 1, d[0], ns, D.out_f[0], d[0], 1, k[0], W, false, sc, kPhBig);
@@ -229,7 +453,8 @@ __global__ void __launch_bounds__(kThreads, 2) leaf_als_kernel(Params prm, const
           s2 = dst;
           t2 ^= 1;
         }
-        llsv_unfold(s2, prod_range(pc, 0, n), d[n], prod_range(pc, n + 1, p), kn, D.out_f[n], G, V, misc, dsm, sc);
+        llsv_unfold(s2, prod_range(pc, 0, n), d[n], prod_range(pc, n + 1, p), kn, D.out_f[n], G, V, misc, dsm, sc,
+                    k[n], D.ws + lay.SI);
         k[n] = kn;
         Pn = s2;
       }
@@ -258,6 +483,8 @@ __global__ void __launch_bounds__(kThreads, 2) leaf_als_kernel(Params prm, const
     D.status[5 + kMaxP] = sc.eig_sweeps;
     sc.cyc[kPhAll] = clock64() - t_kernel;
     for (int i = 0; i < 8; ++i) D.status[6 + kMaxP + i] = int(sc.cyc[i] >> 10);
+    D.status[14 + kMaxP] = sc.si_ok;
+    D.status[15 + kMaxP] = sc.si_fail;
   }
 }
 
@@ -294,7 +521,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   extern __shared__ double dsm[];
   const long long t_kernel = tstart();
   if (threadIdx.x == 0) {
-    sc.eig_calls = sc.eig_sweeps = 0;
+    sc.eig_calls = sc.eig_sweeps = sc.si_ok = sc.si_fail = 0;
     for (int i = 0; i < 8; ++i) sc.cyc[i] = 0;
   }
   const StitchDesc D = descs[blockIdx.x];
@@ -495,7 +722,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           // Z_n += F x_n V_in
           mode_product(src, zo, cur[n], zi, pv.v[n], 1, d[n], d[n], Z, i > 0, sc);
         }
-        llsv_unfold(Z, zo, d[n], zi, kn, D.out_f[n], G, Vg, misc, dsm, sc);
+        llsv_unfold(Z, zo, d[n], zi, kn, D.out_f[n], G, Vg, misc, dsm, sc, k[n], ws + lay.SI);
         k[n] = kn;
         for (int i = 0; i < s; ++i) {
           const PartView pv = load_part(parts[i]);
@@ -622,6 +849,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     D.status[5 + kMaxP] = sc.eig_sweeps;
     sc.cyc[kPhAll] = clock64() - t_kernel;
     for (int i = 0; i < 8; ++i) D.status[6 + kMaxP + i] = int(sc.cyc[i] >> 10);
+    D.status[14 + kMaxP] = sc.si_ok;
+    D.status[15 + kMaxP] = sc.si_fail;
   }
 }
 

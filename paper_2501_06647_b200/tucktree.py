@@ -439,7 +439,8 @@ def kernel_launches() -> int:
 
 def solver_stats() -> dict:
     """Cumulative ALS/eigensolver counters (problems, ALS sweeps, eig calls, Jacobi sweeps)."""
-    out = np.zeros(12, dtype=np.int64)
+    out = np.zeros(14, dtype=np.int64)
     lib().tt_solver_stats(out.ctypes.data_as(i64ptr))
     return dict(zip(("problems", "als_sweeps", "eig_calls", "jacobi_sweeps", "kcyc_eig", "kcyc_gram", "kcyc_ttm",
-                     "kcyc_gemm", "kcyc_ortho_sign", "kcyc_u0", "kcyc_leaf_x", "kcyc_problem"), (int(v) for v in out)))
+                     "kcyc_gemm", "kcyc_ortho_sign", "kcyc_u0", "kcyc_leaf_x", "kcyc_problem", "subspace_ok",
+                     "subspace_fallback"), (int(v) for v in out)))

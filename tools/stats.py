@@ -13,6 +13,7 @@ def show(tag, s0, s1, ms):
     n = max(d["problems"], 1)
     tot = max(d["kcyc_problem"], 1)
     parts = {k[5:]: f"{100 * v / tot:.0f}%" for k, v in d.items() if k.startswith("kcyc") and k != "kcyc_problem"}
+    parts["si_ok/fail"] = f"{d['subspace_ok']}/{d['subspace_fallback']}"
     print(tag, "problems", n, "als/prob %.2f" % (d["als_sweeps"] / n), "jacobi/eig %.2f" % (d["jacobi_sweeps"] / max(d["eig_calls"], 1)),
           "kcyc/prob %.0f" % (tot / n), parts, "ms", [round(v, 3) for v in ms])
 s0 = E.solver_stats(); t.append(x); s1 = E.solver_stats(); show("build", s0, s1, t.last_timing_ms())
