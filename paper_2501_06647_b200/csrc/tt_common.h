@@ -138,7 +138,7 @@ TT_HD LeafWs leaf_ws_layout(int p, int64_t len, const int64_t* d, const int64_t*
 }
 
 struct StitchWs {
-  int64_t P, C, S, E, A, G, V, T1, T2, Z, WK, HH, SI, misc, total, gram_n;
+  int64_t P, C, S, E, A, E2, G, V, T1, T2, Z, WK, HH, SI, misc, total, gram_n;
   int64_t per_part_P, per_part_C, per_part_S, per_part_E;
 };
 
@@ -169,7 +169,8 @@ TT_HD StitchWs stitch_ws_layout(int p, int64_t L, const int64_t* d, const int64_
   w.S = w.C + nparts * w.per_part_C;
   w.E = w.S + nparts * w.per_part_S;
   w.A = w.E + nparts * w.per_part_E;
-  w.G = w.A + nparts * w.per_part_E;
+  w.E2 = w.A + nparts * w.per_part_E;
+  w.G = w.E2 + nparts * w.per_part_E;
   w.V = w.G + g * g;
   w.T1 = w.V + g * g;
   w.T2 = w.T1 + chain;

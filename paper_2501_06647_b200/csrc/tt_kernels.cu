@@ -128,7 +128,9 @@ __device__ void chol_inv_warp(const double* G, int k, double* L, double* Linv, B
       for (int l = 0; l < j; ++l) sdiag -= L[j + l * k] * L[j + l * k];
     }
     sdiag = __shfl_sync(0xffffffffu, sdiag, j);
-    if (!(sdiag > 1e-26 * dmax)) {
+    // A rank-deficient Gram has pivots ~eps*dmax; a basis with condition
+    // number <= ~1e7 keeps them >= 1e-14*dmax. Anything smaller falls back.
+    if (!(sdiag > 1e-14 * dmax)) {
       ok = false;
       break;
     }
@@ -481,7 +483,11 @@ __global__ void __launch_bounds__(kThreads, 2) leaf_als_kernel(Params prm, const
     for (int m = 0; m < kMaxP; ++m) D.status[4 + m] = m < p ? int(k[m]) : 0;
     D.status[4 + kMaxP] = sc.eig_calls;
     D.status[5 + kMaxP] = sc.eig_sweeps;
+#ifdef TT_INSTRUMENT
     sc.cyc[kPhAll] = clock64() - t_kernel;
+#else
+    (void)t_kernel;
+#endif
     for (int i = 0; i < 8; ++i) D.status[6 + kMaxP + i] = int(sc.cyc[i] >> 10);
     D.status[14 + kMaxP] = sc.si_ok;
     D.status[15 + kMaxP] = sc.si_fail;
@@ -553,6 +559,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   auto Sp = [&](int i) { return ws + lay.S + int64_t(i) * lay.per_part_S; };
   auto Ep = [&](int i) { return ws + lay.E + int64_t(i) * lay.per_part_E; };
   auto Ap = [&](int i) { return ws + lay.A + int64_t(i) * lay.per_part_E; };
+  auto E2p = [&](int i) { return ws + lay.E2 + int64_t(i) * lay.per_part_E; };
 
   // ---- partial-hit metric S_i = Vsub^T Vsub and the norm of the implied tensor
   double norm_sq = 0.0;
@@ -613,6 +620,181 @@ __global__ void __launch_bounds__(kThreads, 2)
           tog ^= 1;
         }
       }
+      // ---- subspace iteration on the implicit Z0 in compressed coordinates:
+      // U0 = blockdiag(V_sub,i) E with E^T S E = I; Z0 Z0^T U0 maps to
+      // E <- C (C^T S E). Warm start: the previous sweep's E, or in sweep 0 the
+      // k0 columns of C with the largest S-norm. Rayleigh-Ritz makes E the exact
+      // left singular vectors; any failure falls through to the eigen paths.
+      bool mode0_done = false;
+      int64_t rho0_sum = 0;
+      for (int i = 0; i < s; ++i) rho0_sum += parts[i].rho[0];
+      if (k0n <= kSiMaxK && Q >= 2 * k0n && Q * k0n <= kSiMaxYK && rho0_sum >= k0n) {
+        const long long t_si = tstart();
+        double* Y = wk;                          // Q x k0
+        double* small = ws + lay.SI;             // 4 k x k
+        double* B = small + 4 * k0n * k0n;       // k x k
+        const int kk = int(k0n);
+        auto apply_S = [&](int i, const double* X, double* out) {  // out = S_i X (rho0 x k)
+          const int64_t r0 = parts[i].rho[0];
+          if (parts[i].partial) {
+            gemm(r0, kk, r0, Sp(i), 1, r0, X, 1, r0, out, 1, r0, false, sc);
+          } else if (out != X) {
+            bcopy(out, X, r0 * kk);
+          }
+        };
+        // S-orthonormalise E (two CholeskyQR passes with the metric S)
+        auto s_orth = [&]() -> bool {
+          for (int pass = 0; pass < 2; ++pass) {
+            double* G = small;
+            double* L = small + kk * kk;
+            double* Li = small + 2 * kk * kk;
+            for (int i = 0; i < s; ++i) {
+              const int64_t r0 = parts[i].rho[0];
+              apply_S(i, Ep(i), Ap(i));
+              gemm(kk, kk, r0, Ep(i), r0, 1, Ap(i), 1, r0, G, 1, kk, i > 0, sc);
+            }
+            if (threadIdx.x == 0) sc.ibcast[2] = 0;
+            __syncthreads();
+            chol_inv_warp(G, kk, L, Li, sc);
+            __syncthreads();
+            if (sc.ibcast[2]) return false;
+            for (int i = 0; i < s; ++i) {
+              const int64_t r0 = parts[i].rho[0];
+              double* E = Ep(i);
+              for (int64_t r = threadIdx.x; r < r0; r += blockDim.x) {
+                double w[kSiMaxK];
+#pragma unroll
+                for (int l = 0; l < kSiMaxK; ++l) w[l] = l < kk ? E[r + l * r0] : 0.0;
+                for (int j = 0; j < kk; ++j) {
+                  double v = 0.0;
+#pragma unroll
+                  for (int l = 0; l < kSiMaxK; ++l)
+                    if (l <= j) v = fma(w[l], Li[j + l * kk], v);
+                  E[r + j * r0] = v;
+                }
+              }
+            }
+            __syncthreads();
+          }
+          return true;
+        };
+        bool ok = true;
+        if (sweep == 0 || k[0] < k0n) {
+          // start: the k0 columns of C with the largest S-norm
+          double* cn = misc + kMisc / 2;  // Q norms
+          for (int64_t j = threadIdx.x; j < Q; j += blockDim.x) cn[j] = 0.0;
+          __syncthreads();
+          for (int i = 0; i < s; ++i) {
+            const int64_t r0 = parts[i].rho[0];
+            const double* Ci = Cp(i);
+            for (int64_t j = threadIdx.x; j < Q; j += blockDim.x) {
+              double v = 0.0;
+              if (parts[i].partial) {
+                const double* S = Sp(i);
+                for (int64_t a = 0; a < r0; ++a)
+                  for (int64_t b = 0; b < r0; ++b) v = fma(Ci[a * Q + j] * S[a + b * r0], Ci[b * Q + j], v);
+              } else {
+                for (int64_t a = 0; a < r0; ++a) v = fma(Ci[a * Q + j], Ci[a * Q + j], v);
+              }
+              cn[j] += v;
+            }
+            __syncthreads();
+          }
+          int* pick = reinterpret_cast<int*>(misc);
+          for (int64_t j = threadIdx.x; j < Q; j += blockDim.x) {
+            int rank = 0;
+            for (int64_t l = 0; l < Q; ++l) rank += (cn[l] > cn[j] || (cn[l] == cn[j] && l < j));
+            if (rank < kk) pick[rank] = int(j);
+          }
+          __syncthreads();
+          for (int i = 0; i < s; ++i) {
+            const int64_t r0 = parts[i].rho[0];
+            const double* Ci = Cp(i);
+            double* E = Ep(i);
+            for (int64_t idx = threadIdx.x; idx < r0 * kk; idx += blockDim.x) {
+              const int64_t a = idx % r0, c = idx / r0;
+              E[idx] = Ci[a * Q + pick[c]];
+            }
+          }
+          __syncthreads();
+          ok = s_orth();
+        } else if (k[0] > k0n) {
+          // previous E has more columns (ld rho0): keep the first k0n (same ld)
+          ok = true;
+        }
+        bool conv = false;
+        for (int it = 0; ok && it < kSiMaxIter; ++it) {
+          // A_i = S_i E_i ; Y = sum_i C_i^T A_i (Q x k) ; B = Y^T Y ; W_i = C_i Y
+          for (int i = 0; i < s; ++i) {
+            const int64_t r0 = parts[i].rho[0];
+            apply_S(i, Ep(i), Ap(i));
+            gemm(Q, kk, r0, Cp(i), 1, Q, Ap(i), 1, r0, Y, 1, Q, i > 0, sc);
+          }
+          gram_tall(Y, Q, Q, kk, B);
+          double rsq = 0.0;
+          for (int i = 0; i < s; ++i) {
+            const int64_t r0 = parts[i].rho[0];
+            gemm(r0, kk, Q, Cp(i), Q, 1, Y, 1, Q, E2p(i), 1, r0, false, sc);
+            // R = W - E B (into T[0]); rsq += <R, S R>
+            double* R = T[0];
+            for (int64_t idx = threadIdx.x; idx < r0 * kk; idx += blockDim.x) {
+              const int64_t a = idx % r0, j = idx / r0;
+              double v = E2p(i)[idx];
+              for (int l = 0; l < kk; ++l) v = fma(-Ep(i)[a + l * r0], B[l + j * kk], v);
+              R[idx] = v;
+            }
+            __syncthreads();
+            double part = 0.0;
+            if (parts[i].partial) {
+              gemm(r0, kk, r0, Sp(i), 1, r0, R, 1, r0, HH, 1, r0, false, sc);
+              for (int64_t idx = threadIdx.x; idx < r0 * kk; idx += blockDim.x) part = fma(R[idx], HH[idx], part);
+            } else {
+              for (int64_t idx = threadIdx.x; idx < r0 * kk; idx += blockDim.x) part = fma(R[idx], R[idx], part);
+            }
+            rsq += block_sum(part, sc);
+          }
+          double bsq = 0.0;
+          for (int e = threadIdx.x; e < kk * kk; e += blockDim.x) bsq = fma(B[e], B[e], bsq);
+          bsq = block_sum(bsq, sc);
+          if (!(bsq > 0.0)) {
+            ok = false;
+            break;
+          }
+          if (rsq <= 1e-26 * bsq) {
+            conv = true;
+            break;
+          }
+          for (int i = 0; i < s; ++i) bcopy(Ep(i), E2p(i), parts[i].rho[0] * kk);
+          ok = s_orth();
+        }
+        if (ok && conv) {
+          // Rayleigh-Ritz: E <- E R (descending), then A_i = S_i E_i
+          int* order = reinterpret_cast<int*>(misc);
+          double* diag = nullptr;
+          const double* R = eig_run(B, kk, small, order, dsm, &diag, sc);
+          for (int i = 0; i < s; ++i) {
+            const int64_t r0 = parts[i].rho[0];
+            double* E = Ep(i);
+            double* E2 = E2p(i);
+            for (int64_t idx = threadIdx.x; idx < r0 * kk; idx += blockDim.x) {
+              const int64_t a = idx % r0, j = idx / r0;
+              const double* rj = R + int64_t(order[j]) * kk;
+              double v = 0.0;
+              for (int l = 0; l < kk; ++l) v = fma(E[a + l * r0], rj[l], v);
+              E2[idx] = v;
+            }
+            __syncthreads();
+            bcopy(E, E2, r0 * kk);
+            if (parts[i].partial) apply_S(i, E, Ap(i));
+          }
+          any_zero_sigma = 0;
+          mode0_done = true;
+          if (threadIdx.x == 0) sc.si_ok += 1;
+        } else if (threadIdx.x == 0) {
+          sc.si_fail += 1;
+        }
+        tstop(sc, kPhEig, t_si);
+      }
       // Row-compressed variant: with entire parts only, Z0 = blockdiag(V_i0) C
       // (C = [C_1; ...; C_s], sum rho_i0 rows) and V_i0 orthonormal, so the left
       // singular vectors of Z0 are blockdiag(V_i0) times the eigenvectors of
@@ -624,7 +806,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         rsum += parts[i].rho[0];
         all_entire = all_entire && !parts[i].partial;
       }
-      if (all_entire && rsum < Q && k0n <= rsum) {  // else: rank-deficient Z0 needs the completion path
+      if (mode0_done) {
+        // E_i, A_i already set by the subspace iteration
+      } else if (all_entire && rsum < Q && k0n <= rsum) {  // else: rank-deficient Z0 needs the completion path
         int64_t oi = 0;
         for (int i = 0; i < s; ++i) {
           const int64_t ri = parts[i].rho[0];
@@ -847,7 +1031,11 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int m = 0; m < kMaxP; ++m) D.status[4 + m] = m < p ? int(k[m]) : 0;
     D.status[4 + kMaxP] = sc.eig_calls;
     D.status[5 + kMaxP] = sc.eig_sweeps;
+#ifdef TT_INSTRUMENT
     sc.cyc[kPhAll] = clock64() - t_kernel;
+#else
+    (void)t_kernel;
+#endif
     for (int i = 0; i < 8; ++i) D.status[6 + kMaxP + i] = int(sc.cyc[i] >> 10);
     D.status[14 + kMaxP] = sc.si_ok;
     D.status[15 + kMaxP] = sc.si_fail;
