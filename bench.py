@@ -206,7 +206,8 @@ def run_engine(args, rank, world, local_rank):
         torch.cuda.synchronize()
     launches = eng.kernel_launches() - launches0
     stats1 = eng.solver_stats()
-    solver = {k: (stats1[k] - stats0[k]) / args.steps for k in stats0}
+    solver = {k: (stats1[k] - stats0[k]) / args.steps for k in ("problems", "als_sweeps", "eig_calls", "jacobi_sweeps",
+                                                                "subspace_ok", "subspace_fallback", "subspace_iters")}
     span_ms = ev0.elapsed_time(ev1)
     if dist:
         dist.barrier()

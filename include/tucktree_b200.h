@@ -211,8 +211,11 @@ int64_t tt_kernel_launches(void);
  * [4..11] thousands of SM cycles summed over problems in: eigen-solves, Gram
  * matrices (+U assembly), small mode products, small GEMMs, orthonormalise +
  * sign fix, U_0 materialisation, leaf X passes, whole problem; [12..13]
- * subspace-iteration solves that converged / fell back to Jacobi.         */
-void tt_solver_stats(int64_t* out14);
+ * subspace-iteration solves that converged / fell back to Jacobi, [14]
+ * subspace iterations, [15..18] kcycles inside subspace iteration (A^T U,
+ * A Y + residual, CholeskyQR2, Rayleigh-Ritz). Entries [0..18] count leaf
+ * (tucker_als) problems, [19..37] stitch problems.                        */
+void tt_solver_stats(int64_t* out38);
 
 #ifdef __cplusplus
 }

@@ -29,12 +29,14 @@ struct BlockScratch {
   int jp[256], jq[256];
   int rotated[2];
   int eig_calls, eig_sweeps;  // instrumentation (Jacobi sweeps per problem)
-  int si_ok, si_fail;         // subspace-iteration outcomes
-  long long cyc[8];           // instrumentation: cycles per phase (see kPhase*)
+  int si_ok, si_fail, si_iters;  // subspace-iteration outcomes and iterations
+  long long cyc[12];          // instrumentation: cycles per phase (see kPh*, kSi*)
 };
 
 // Phase-timer slots (thread 0 accumulates clock64 deltas; instrumentation).
 enum { kPhEig = 0, kPhGram = 1, kPhTtm = 2, kPhGemm = 3, kPhOrtho = 4, kPhU0 = 5, kPhBig = 6, kPhAll = 7 };
+// subspace-iteration internals (subsets of kPhEig): A^T U + Gram, A Y + residual, CholeskyQR2, Rayleigh-Ritz
+enum { kSiAtU = 8, kSiAY = 9, kSiQR = 10, kSiRR = 11 };
 #ifdef TT_INSTRUMENT
 __device__ __forceinline__ long long tstart() { return threadIdx.x == 0 ? clock64() : 0; }
 __device__ __forceinline__ void tstop(BlockScratch& sc, int slot, long long t0) {
@@ -99,6 +101,51 @@ __device__ __forceinline__ double bsumsq(const double* __restrict__ x, int64_t n
   double s = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s = fma(x[i], x[i], s);
   return block_sum(s, sc);
+}
+
+// ---------------------------------------------------------------------------
+// TMA bulk-copy (cp.async.bulk) + mbarrier helpers for streaming global memory
+// through a shared-memory ring (sm_90+; the B200 bulk-copy engine).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "TT_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra TT_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
 }
 
 // ---------------------------------------------------------------------------

@@ -49,8 +49,23 @@ TT_HD int64_t stitch_mode_rank(int p, const int64_t* d, const int64_t* rc, const
 
 // ---------------------------------------------------------------------------
 // Problem descriptors (device-visible PODs).
+// Tile shape of the streamed mode products (shared by the host, which encodes
+// the TMA tensor maps, and the device loop): G slabs x cj rows x tw columns.
+struct StreamTile {
+  int64_t tw, G, cj;
+};
+constexpr int64_t kStreamTileDoubles = 2560;  // 20 KB per ring stage
+TT_HD StreamTile stream_tile(int64_t outer, int64_t d, int64_t inner) {
+  StreamTile t;
+  t.tw = imin(inner, 256);
+  t.G = imax(1, imin(imin(outer, 256 / t.tw), 256));
+  t.cj = imax(1, imin(imin(d, kStreamTileDoubles / (t.G * t.tw)), 256));
+  return t;
+}
+
 struct LeafDesc {
   const double* x;                 // row-major (len, D_1, ..., D_{p-1})
+  const void* tmaps;               // 2 CUtensorMaps (128 B each): [0] X as (inner, D_1, len), [1] X as (ns, len); or null
   int64_t len;                     // temporal extent of this block
   const double* init[kMaxP];       // init factors for this length (D_n x rc_n, col-major)
   double* out_f[kMaxP];            // output factor slots (ld = D_n; factor 0: ld = len)
@@ -91,7 +106,7 @@ struct Params {
   const double* stitch_init[kMaxP];  // stitch init factors U_m (m >= 1), D_m x rc_m
 };
 
-constexpr int kStatusInts = 4 + kMaxP + 12;  // ..., eig calls, Jacobi sweeps, kcycles[8], subspace ok/fail
+constexpr int kStatusInts = 4 + kMaxP + 17;  // ..., eig calls, Jacobi sweeps, kcycles[8], subspace ok/fail
 
 // ---------------------------------------------------------------------------
 // Workspace layouts (in doubles). The misc tail holds reductions, sigma, order.

@@ -6,6 +6,8 @@
 // touched sets, factor column counts); the device owns every floating-point
 // operation. There is no CPU numeric fallback: without a working CUDA device
 // every numeric entry point fails with TT_ECUDA.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -38,7 +40,7 @@ namespace {
 
 thread_local std::string g_err;
 // problems, ALS sweeps, eig calls, Jacobi sweeps (cumulative, all trees)
-int64_t g_stats[14] = {};
+int64_t g_stats[2][19] = {};  // [0] leaf problems, [1] stitch problems
 
 struct TTError : std::runtime_error {
   tt_status code;
@@ -216,7 +218,7 @@ struct DeviceGuard {
 struct Exec {
   int device = 0;
   cudaStream_t stream = nullptr;
-  DevBuf d_desc, d_parts, d_ws, d_status, d_obj, d_stage;
+  DevBuf d_desc, d_parts, d_ws, d_status, d_obj, d_stage, d_tmaps;
   std::vector<char> h_status_bytes;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   explicit Exec(int dev) : device(dev) {
@@ -239,6 +241,54 @@ struct ProblemStatus {
   std::vector<double> objective;
 };
 
+// TMA tensor maps for the two streamed passes over a leaf block X (row-major
+// (len, D_1, rest)): [0] X as 3-D (rest, D_1, len) for Y = X x_1 U_1^T, [1] X as
+// 2-D (ns, len) for W = X x_0 U_0^T. Box shapes come from stream_tile(), the
+// same function the kernel's tile loop uses. Returns false when the layout is
+// not TMA-compatible (16-byte strides/box rows); the kernel then falls back.
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+bool encode_leaf_maps(const double* x, Index len, Index d1, Index rest, CUtensorMap* out) {
+  auto enc = tensor_map_encoder();
+  if (!enc || (reinterpret_cast<uintptr_t>(x) & 15u) != 0) return false;
+  const Index ns = d1 * rest;
+  const StreamTile ta = stream_tile(len, d1, rest), tb = stream_tile(1, len, ns);
+  if ((rest * 8) % 16 || (ta.tw * 8) % 16 || (tb.tw * 8) % 16) return false;
+  {
+    const cuuint64_t dims[3] = {cuuint64_t(rest), cuuint64_t(d1), cuuint64_t(len)};
+    const cuuint64_t strides[2] = {cuuint64_t(rest * 8), cuuint64_t(d1 * rest * 8)};
+    const cuuint32_t box[3] = {cuuint32_t(ta.tw), cuuint32_t(ta.cj), cuuint32_t(ta.G)};
+    const cuuint32_t es[3] = {1, 1, 1};
+    if (enc(&out[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(x), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  {
+    const cuuint64_t dims[2] = {cuuint64_t(ns), cuuint64_t(len)};
+    const cuuint64_t strides[1] = {cuuint64_t(ns * 8)};
+    const cuuint32_t box[2] = {cuuint32_t(tb.tw), cuuint32_t(tb.cj)};
+    const cuuint32_t es[2] = {1, 1};
+    if (enc(&out[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(x), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  return true;
+}
+
 // Uploads descriptors, runs a leaf batch, reads statuses back (synchronous).
 std::vector<ProblemStatus> run_leaf_batch(Exec& ex, const Params& prm, std::vector<LeafDesc>& descs,
                                           const std::vector<Index>& ws_sizes) {
@@ -256,6 +306,20 @@ std::vector<ProblemStatus> run_leaf_batch(Exec& ex, const Params& prm, std::vect
     off += static_cast<size_t>(ws_sizes[i]);
     descs[i].status = ex.d_status.as<int32_t>() + size_t(i) * kStatusInts;
     descs[i].objective = ex.d_obj.as<double>() + size_t(i) * prm.max_iters;
+  }
+  // TMA tensor maps (two per leaf, 64-byte aligned) for the streamed X passes
+  if (prm.p >= 2) {
+    std::vector<CUtensorMap> maps(size_t(2) * n);
+    ex.d_tmaps.ensure(sizeof(CUtensorMap) * 2 * n + 128);
+    CUtensorMap* dmaps = reinterpret_cast<CUtensorMap*>((reinterpret_cast<uintptr_t>(ex.d_tmaps.p) + 127) & ~uintptr_t(127));
+    for (int i = 0; i < n; ++i) {
+      const Index rest = prod_range(prm.d, 2, prm.p);
+      const bool ok = encode_leaf_maps(descs[i].x, descs[i].len, prm.d[1], rest, &maps[2 * i]);
+      descs[i].tmaps = ok ? static_cast<const void*>(dmaps + 2 * i) : nullptr;
+    }
+    cuda_check(cudaMemcpyAsync(dmaps, maps.data(), sizeof(CUtensorMap) * maps.size(), cudaMemcpyHostToDevice,
+                               ex.stream),
+               "upload tensor maps");
   }
   ex.d_desc.ensure(sizeof(LeafDesc) * n);
   cuda_check(cudaMemcpyAsync(ex.d_desc.p, descs.data(), sizeof(LeafDesc) * n, cudaMemcpyHostToDevice, ex.stream),
@@ -277,13 +341,15 @@ std::vector<ProblemStatus> run_leaf_batch(Exec& ex, const Params& prm, std::vect
     for (int m = 0; m < kMaxP; ++m) st[i].k[m] = s[4 + m];
     st[i].eig_calls = s[4 + kMaxP];
     st[i].eig_sweeps = s[5 + kMaxP];
-    g_stats[0] += 1;
-    g_stats[1] += s[0];
-    g_stats[2] += s[4 + kMaxP];
-    g_stats[3] += s[5 + kMaxP];
-    for (int q = 0; q < 8; ++q) g_stats[4 + q] += s[6 + kMaxP + q];
-    g_stats[12] += s[14 + kMaxP];
-    g_stats[13] += s[15 + kMaxP];
+    g_stats[0][0] += 1;
+    g_stats[0][1] += s[0];
+    g_stats[0][2] += s[4 + kMaxP];
+    g_stats[0][3] += s[5 + kMaxP];
+    for (int q = 0; q < 8; ++q) g_stats[0][4 + q] += s[6 + kMaxP + q];
+    g_stats[0][12] += s[14 + kMaxP];
+    g_stats[0][13] += s[15 + kMaxP];
+    g_stats[0][14] += s[16 + kMaxP];
+    for (int q = 0; q < 4; ++q) g_stats[0][15 + q] += s[17 + kMaxP + q];
     st[i].objective.assign(ho.begin() + size_t(i) * prm.max_iters, ho.begin() + size_t(i) * prm.max_iters + s[0]);
   }
   return st;
@@ -331,13 +397,15 @@ std::vector<ProblemStatus> run_stitch_batch(Exec& ex, const Params& prm, std::ve
     for (int m = 0; m < kMaxP; ++m) st[i].k[m] = s[4 + m];
     st[i].eig_calls = s[4 + kMaxP];
     st[i].eig_sweeps = s[5 + kMaxP];
-    g_stats[0] += 1;
-    g_stats[1] += s[0];
-    g_stats[2] += s[4 + kMaxP];
-    g_stats[3] += s[5 + kMaxP];
-    for (int q = 0; q < 8; ++q) g_stats[4 + q] += s[6 + kMaxP + q];
-    g_stats[12] += s[14 + kMaxP];
-    g_stats[13] += s[15 + kMaxP];
+    g_stats[1][0] += 1;
+    g_stats[1][1] += s[0];
+    g_stats[1][2] += s[4 + kMaxP];
+    g_stats[1][3] += s[5 + kMaxP];
+    for (int q = 0; q < 8; ++q) g_stats[1][4 + q] += s[6 + kMaxP + q];
+    g_stats[1][12] += s[14 + kMaxP];
+    g_stats[1][13] += s[15 + kMaxP];
+    g_stats[1][14] += s[16 + kMaxP];
+    for (int q = 0; q < 4; ++q) g_stats[1][15 + q] += s[17 + kMaxP + q];
     st[i].objective.assign(ho.begin() + size_t(i) * prm.max_iters, ho.begin() + size_t(i) * prm.max_iters + s[0]);
   }
   return st;
@@ -715,8 +783,9 @@ extern "C" {
 const char* tt_last_error(void) { return g_err.c_str(); }
 const char* tt_version(void) { return "tucktree_b200 0.1 (sm_100a)"; }
 int64_t tt_kernel_launches(void) { return launches(); }
-void tt_solver_stats(int64_t* out14) {
-  for (int i = 0; i < 14; ++i) out14[i] = g_stats[i];
+void tt_solver_stats(int64_t* out38) {
+  for (int k = 0; k < 2; ++k)
+    for (int i = 0; i < 19; ++i) out38[k * 19 + i] = g_stats[k][i];
 }
 
 tt_status tt_tree_create(const tt_config* cfg, tt_tree** out) {

@@ -22,6 +22,161 @@ namespace ttb {
 constexpr int kEigSmemN = 64;  // Jacobi runs in shared memory up to this size
 constexpr size_t kDynSmem = size_t(2) * kEigSmemN * kEigSmemN * sizeof(double);
 
+// Leaf streaming ring: kStages tiles of kTileD doubles, plus U^T staging.
+constexpr int kStages = 3;
+constexpr int kTileD = int(kStreamTileDoubles);   // 20 KB per stage
+constexpr int kUStage = 4096;  // U^T staged in shared memory when d*r <= this (32 KB)
+constexpr size_t kLeafDynSmem = size_t(kStages * kTileD + kUStage) * sizeof(double);  // 96 KB
+
+struct Pipe {
+  uint64_t full[kStages];
+  uint32_t uses[kStages];  // completed fills per stage (phase parity)
+};
+
+// out[o][a][t] = sum_j U[j][a] in[o][j][t]  (in: row-major (outer, d, inner);
+// U: d x r col-major, ld d; r <= 16), streaming `in` from global memory through
+// a kStages-deep cp.async.bulk ring. A tile is (G slabs) x (cj rows of j) x
+// (tw columns of t); each thread owns one output column (g, t) and keeps its r
+// accumulators across the j-tiles. Optionally accumulates sum(in^2) (every
+// element is consumed by exactly one thread). Requires 16-byte aligned rows
+// (inner*8 and tw*8 multiples of 16, 16-aligned base).
+template <int R>
+__device__ __noinline__ void ttm_stream_r(const double* __restrict__ in, int64_t outer, int64_t d, int64_t inner,
+                                          const double* __restrict__ U, double* __restrict__ out, double* dyn,
+                                          Pipe& pp, double* norm_acc, const void* tmap, int tmap_rank) {
+  constexpr int r = R;
+  const StreamTile tile = stream_tile(outer, d, inner);
+  const int64_t tw = tile.tw, G = tile.G, cj = tile.cj;
+  const int64_t ngrp = (outer + G - 1) / G, ntt = (inner + tw - 1) / tw, njt = (d + cj - 1) / cj;
+  const int64_t ntiles = ngrp * ntt * njt;
+  double* ring = dyn;
+  double* Ut = dyn + kStages * kTileD;
+  const bool u_smem = d * r <= kUStage;
+  if (u_smem) {  // U^T, j-major: Ut[j*r + a]
+    for (int64_t idx = threadIdx.x; idx < d * r; idx += blockDim.x) {
+      const int64_t j = idx / r, a = idx - j * r;
+      Ut[idx] = U[j + a * d];
+    }
+  }
+  fence_proxy_async();  // prior generic smem accesses vs. the bulk-copy writes below
+  __syncthreads();
+  auto issue = [&](int64_t t) {  // warp 0: fill the stage of tile t
+    const int st = int(t % kStages);
+    const int64_t jt = t % njt, rest = t / njt, tt = rest % ntt, grp = rest / ntt;
+    const int64_t o0 = grp * G, g_n = imin(G, outer - o0);
+    const int64_t j0 = jt * cj, jn = imin(cj, d - j0);
+    const int64_t t0 = tt * tw, tn = imin(tw, inner - t0);
+    double* dst = ring + int64_t(st) * kTileD;
+    const int lane = threadIdx.x & 31;
+    if (tmap != nullptr) {
+      // one TMA box per tile: (tw, cj, G) over (t, j, o); out-of-bounds parts are
+      // zero-filled and still count toward the transaction bytes
+      if (lane == 0) {
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&pp.full[st], uint32_t(G * cj * tw * sizeof(double)));
+        if (tmap_rank == 3)
+          tma_load_3d(dst, tmap, int(t0), int(j0), int(o0), &pp.full[st]);
+        else
+          tma_load_2d(dst, tmap, int(t0), int(j0), &pp.full[st]);
+      }
+      (void)g_n;
+      (void)jn;
+      (void)tn;
+      return;
+    }
+    const bool whole_rows = (tn == inner);  // one contiguous segment per slab
+    const int64_t nseg = whole_rows ? g_n : g_n * jn;
+    const uint32_t seg_bytes = uint32_t((whole_rows ? jn * inner : tn) * sizeof(double));
+    if (lane == 0) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&pp.full[st], uint32_t(nseg) * seg_bytes);
+    }
+    __syncwarp();
+    for (int64_t sg = lane; sg < nseg; sg += 32) {
+      int64_t g, jj;
+      if (whole_rows) {
+        g = sg;
+        jj = 0;
+      } else {
+        g = sg / jn;
+        jj = sg - g * jn;
+      }
+      const double* src = in + ((o0 + g) * d + j0 + jj) * inner + t0;
+      bulk_g2s(dst + (g * cj + jj) * tw, src, seg_bytes, &pp.full[st]);
+    }
+  };
+  if (threadIdx.x < 32)
+    for (int64_t t = 0; t < imin(int64_t(kStages), ntiles); ++t) issue(t);
+  double acc[R];
+  double nrm = 0.0;
+  for (int64_t t = 0; t < ntiles; ++t) {
+    const int st = int(t % kStages);
+    const int64_t jt = t % njt, rest = t / njt, tt = rest % ntt, grp = rest / ntt;
+    const int64_t o0 = grp * G, g_n = imin(G, outer - o0);
+    const int64_t j0 = jt * cj, jn = imin(cj, d - j0);
+    const int64_t t0 = tt * tw, tn = imin(tw, inner - t0);
+    const int64_t g = threadIdx.x / tw, tl = threadIdx.x - g * tw;
+    const bool active = threadIdx.x < G * tw && g < g_n && tl < tn;
+    if (jt == 0) {
+#pragma unroll
+      for (int a = 0; a < R; ++a) acc[a] = 0.0;
+    }
+    mbar_wait(&pp.full[st], pp.uses[st] & 1u);
+    if (active) {
+      // whole-row tiles are packed with row length inner == tn
+      const double* x = ring + int64_t(st) * kTileD + g * cj * tw + tl;
+      if (u_smem) {
+        for (int64_t jj = 0; jj < jn; ++jj) {
+          const double xv = x[jj * tw];
+          if (norm_acc) nrm = fma(xv, xv, nrm);
+          const double* ur = Ut + (j0 + jj) * R;
+#pragma unroll
+          for (int a = 0; a < R; ++a) acc[a] = fma(ur[a], xv, acc[a]);
+        }
+      } else {
+        for (int64_t jj = 0; jj < jn; ++jj) {
+          const double xv = x[jj * tw];
+          if (norm_acc) nrm = fma(xv, xv, nrm);
+#pragma unroll
+          for (int a = 0; a < R; ++a) acc[a] = fma(__ldg(U + (j0 + jj) + a * d), xv, acc[a]);
+        }
+      }
+      if (jt == njt - 1) {
+        double* dst = out + (o0 + g) * r * inner + t0 + tl;
+#pragma unroll
+        for (int a = 0; a < R; ++a) dst[a * inner] = acc[a];
+      }
+    }
+    fence_proxy_async();
+    __syncthreads();  // every thread is done with stage st
+    if (threadIdx.x == 0) pp.uses[st] += 1;
+    if (threadIdx.x < 32 && t + kStages < ntiles) issue(t + kStages);
+  }
+  if (norm_acc) *norm_acc += nrm;
+  __syncthreads();
+}
+
+__device__ __forceinline__ void ttm_stream(const double* in, int64_t outer, int64_t d, int64_t inner, const double* U,
+                                           int r, double* out, double* dyn, Pipe& pp, double* norm_acc,
+                                           const void* tmap, int tmap_rank) {
+  switch (r) {
+#define TT_CASE(N) \
+  case N:          \
+    ttm_stream_r<N>(in, outer, d, inner, U, out, dyn, pp, norm_acc, tmap, tmap_rank); \
+    break;
+    TT_CASE(1) TT_CASE(2) TT_CASE(3) TT_CASE(4) TT_CASE(5) TT_CASE(6) TT_CASE(7) TT_CASE(8)
+    TT_CASE(9) TT_CASE(10) TT_CASE(11) TT_CASE(12) TT_CASE(13) TT_CASE(14) TT_CASE(15) TT_CASE(16)
+#undef TT_CASE
+    default:
+      break;
+  }
+}
+
+__device__ __forceinline__ bool stream_ok(const double* in, int64_t inner, int r) {
+  const int64_t tw = imin(inner, 256);
+  return r <= 16 && ((reinterpret_cast<uintptr_t>(in) & 15u) == 0) && ((inner * 8) % 16 == 0) && ((tw * 8) % 16 == 0);
+}
+
 // Thread-per-output-element mode product, for shapes with few output columns.
 __device__ __forceinline__ void ttm_elems(const double* __restrict__ in, int64_t outer, int64_t d, int64_t inner,
                                           const double* __restrict__ M, int64_t ms_a, int64_t ms_j, int64_t r,
@@ -158,28 +313,27 @@ __device__ void chol_inv_warp(const double* G, int k, double* L, double* Linv, B
   }
 }
 
-// W (rows x k, ld rows) <- W L^{-T}, where W^T W = L L^T (one CholeskyQR pass).
-__device__ bool cholqr_pass(double* W, int64_t rows, int k, double* small, BlockScratch& sc) {
+// W (rows x K, ld rows) <- W L^{-T}, where W^T W = L L^T (one CholeskyQR pass).
+template <int K>
+__device__ __noinline__ bool cholqr_pass_k(double* W, int64_t rows, double* small, BlockScratch& sc) {
   double* G = small;
-  double* L = small + k * k;
-  double* Li = small + 2 * k * k;
-  gram_tall(W, rows, rows, k, G);
+  double* L = small + K * K;
+  double* Li = small + 2 * K * K;
+  gram_tall(W, rows, rows, K, G);
   if (threadIdx.x == 0) sc.ibcast[2] = 0;
   __syncthreads();
-  chol_inv_warp(G, k, L, Li, sc);
+  chol_inv_warp(G, K, L, Li, sc);
   __syncthreads();
   if (sc.ibcast[2]) return false;
   for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) {
-    double w[kSiMaxK];
+    double w[K];
 #pragma unroll
-    for (int l = 0; l < kSiMaxK; ++l) w[l] = l < k ? W[r + l * rows] : 0.0;
+    for (int l = 0; l < K; ++l) w[l] = W[r + l * rows];
 #pragma unroll
-    for (int j = 0; j < kSiMaxK; ++j) {
-      if (j >= k) break;
+    for (int j = 0; j < K; ++j) {
       double v = 0.0;
 #pragma unroll
-      for (int l = 0; l < kSiMaxK; ++l)
-        if (l <= j) v = fma(w[l], Li[j + l * k], v);
+      for (int l = 0; l <= j; ++l) v = fma(w[l], Li[j + l * K], v);
       W[r + j * rows] = v;
     }
   }
@@ -187,131 +341,164 @@ __device__ bool cholqr_pass(double* W, int64_t rows, int k, double* small, Block
   return true;
 }
 
-// Y (cols x k) = A^T U with A(i, c) = P[offc[c] + i*inner]; split over warps by
-// row chunks, partial sums reduced through shared memory (cols*k <= 1024).
-__device__ void unfold_At_U(const double* __restrict__ P, const int* __restrict__ offc, int64_t rows, int64_t inner,
-                            int cols, const double* __restrict__ U, int k, double* __restrict__ Y, double* part,
-                            BlockScratch& sc) {
-  constexpr int OPL = kSiMaxYK / 32;  // outputs per lane
+// Y (cols x K) = A^T U with A(i, c) = P[offc[c] + i*inner]: warps split the
+// rows, each lane keeps up to 16 outputs in registers (row-outer loop, so the
+// loads of a row are independent), partials reduced through shared memory.
+template <int K>
+__device__ __noinline__ void unfold_At_U_k(const double* __restrict__ P, const int* __restrict__ offc, int64_t rows,
+                                           int64_t inner, int cols, const double* __restrict__ U,
+                                           double* __restrict__ Y, double* part) {
+  constexpr int OPL = 16;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = int(blockDim.x >> 5);
-  const int ne = cols * k;
+  const int ne = cols * K;
   const int64_t chunk = (rows + nw - 1) / nw;
   const int64_t i0 = warp * chunk, i1 = imin(rows, i0 + chunk);
-  double acc[OPL];
-  int oc[OPL], oj[OPL];
+  for (int e0 = 0; e0 < ne; e0 += 32 * OPL) {
+    double acc[OPL];
+    int oc[OPL], oj[OPL];
 #pragma unroll
-  for (int u = 0; u < OPL; ++u) {
-    const int e = lane + 32 * u;
-    const int c = e < ne ? e % cols : 0;
-    oc[u] = offc[c];
-    oj[u] = e < ne ? e / cols : 0;
-    acc[u] = 0.0;
+    for (int u = 0; u < OPL; ++u) {
+      const int e = e0 + lane + 32 * u;
+      const int ee = e < ne ? e : 0;
+      oc[u] = offc[ee % cols];
+      oj[u] = (ee / cols) * int(rows);
+      acc[u] = 0.0;
+    }
+    const int nu = imin(OPL, (ne - e0 - lane + 31) / 32);
+    for (int64_t i = i0; i < i1; ++i) {
+      const double* Pi = P + i * inner;
+      const double* Ui = U + i;
+#pragma unroll
+      for (int u = 0; u < OPL; ++u)
+        if (u < nu) acc[u] = fma(Pi[oc[u]], Ui[oj[u]], acc[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < OPL; ++u) {
+      const int e = e0 + lane + 32 * u;
+      if (u < nu && e < ne) part[warp * ne + e] = acc[u];
+    }
   }
-  for (int64_t i = i0; i < i1; ++i) {
-    const double* Pi = P + i * inner;
-    const double* Ui = U + i;
-#pragma unroll
-    for (int u = 0; u < OPL; ++u)
-      if (lane + 32 * u < ne) acc[u] = fma(Pi[oc[u]], Ui[int64_t(oj[u]) * rows], acc[u]);
-  }
-#pragma unroll
-  for (int u = 0; u < OPL; ++u)
-    if (lane + 32 * u < ne) part[warp * ne + lane + 32 * u] = acc[u];
   __syncthreads();
   for (int e = threadIdx.x; e < ne; e += blockDim.x) {
     double v = 0.0;
     for (int w = 0; w < nw; ++w) v += part[w * ne + e];
-    Y[(e % cols) + int64_t(e / cols) * cols] = v;
+    Y[e] = v;  // e = c + j*cols: column-major cols x K
   }
   __syncthreads();
 }
 
-__device__ bool llsv_subspace(const double* P, int64_t outer, int64_t rows, int64_t inner, int k, int kprev, double* U,
-                              double* si, double* dsm, double* misc, BlockScratch& sc) {
+template <int K>
+__device__ __noinline__ int llsv_subspace_k(const double* P, int64_t outer, int64_t rows, int64_t inner, int kprev,
+                                            double* U, double* si, double* dsm, double* misc, BlockScratch& sc) {
   const int cols = int(outer * inner);
-  double* W = si;                          // rows x k
-  double* Y = W + rows * k;                // cols x k
-  double* small = Y + int64_t(cols) * k;   // 4 k x k
-  double* B = small + 4 * k * k;           // k x k
-  int* offc = reinterpret_cast<int*>(B + k * k);
-  for (int c = threadIdx.x; c < cols; c += blockDim.x)
-    offc[c] = int((c / inner) * rows * inner + (c % inner));
-  // warm start: the current factor's columns, padded with canonical vectors
-  if (kprev < k) {
-    for (int64_t idx = threadIdx.x; idx < rows * (k - kprev); idx += blockDim.x) {
+  // shared-memory carve-up: [0, 4096) partial sums / eigensolver scratch,
+  // then Y (cols x K), the small K x K matrices and the column-offset table
+  double* W = si;                          // rows x K (global workspace)
+  double* Y = dsm + 4096;                  // cols x K   (<= 512)
+  double* small = Y + kSiMaxYK;            // 4 K x K
+  double* B = small + 4 * K * K;           // K x K
+  int* offc = reinterpret_cast<int*>(B + K * K);  // <= 512 ints
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) offc[c] = int((c / inner) * rows * inner + (c % inner));
+  if (kprev < K) {  // warm start padded with canonical vectors
+    for (int64_t idx = threadIdx.x; idx < rows * (K - kprev); idx += blockDim.x) {
       const int64_t r = idx % rows, c = kprev + idx / rows;
       U[r + c * rows] = (r == (c * 7919) % rows) ? 1.0 : 0.0;
     }
     __syncthreads();
-    if (!cholqr_pass(U, rows, k, small, sc) || !cholqr_pass(U, rows, k, small, sc)) return false;
+    if (!cholqr_pass_k<K>(U, rows, small, sc) || !cholqr_pass_k<K>(U, rows, small, sc)) return -1;
   } else {
     __syncthreads();
   }
-  bool conv = false;
+  int iters = -1;
   for (int it = 0; it < kSiMaxIter; ++it) {
-    unfold_At_U(P, offc, rows, inner, cols, U, k, Y, dsm, sc);
-    gram_tall(Y, cols, cols, k, B);
-    // W = A Y (row-parallel, k outputs per row)
+    long long tp = tstart();
+    unfold_At_U_k<K>(P, offc, rows, inner, cols, U, Y, dsm);
+    gram_tall(Y, cols, cols, K, B);
+    tstop(sc, kSiAtU, tp);
+    tp = tstart();
+    double rsq = 0.0;
     for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
-      double acc[kSiMaxK];
+      double acc[K], u[K];
 #pragma unroll
-      for (int j = 0; j < kSiMaxK; ++j) acc[j] = 0.0;
+      for (int j = 0; j < K; ++j) {
+        acc[j] = 0.0;
+        u[j] = U[i + j * rows];
+      }
       const double* Pi = P + i * inner;
       for (int c = 0; c < cols; ++c) {
         const double a = Pi[offc[c]];
 #pragma unroll
-        for (int j = 0; j < kSiMaxK; ++j)
-          if (j < k) acc[j] = fma(a, Y[c + j * cols], acc[j]);
+        for (int j = 0; j < K; ++j) acc[j] = fma(a, Y[c + j * cols], acc[j]);
       }
 #pragma unroll
-      for (int j = 0; j < kSiMaxK; ++j)
-        if (j < k) W[i + j * rows] = acc[j];
-    }
-    __syncthreads();
-    double rsq = 0.0, bsq = 0.0;
-    for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
-      for (int j = 0; j < k; ++j) {
-        double v = W[i + j * rows];
-        for (int l = 0; l < k; ++l) v = fma(-U[i + l * rows], B[l + j * k], v);
+      for (int j = 0; j < K; ++j) {
+        W[i + j * rows] = acc[j];
+        double v = acc[j];  // residual (W - U B)[i, j]
+#pragma unroll
+        for (int l = 0; l < K; ++l) v = fma(-u[l], B[l + j * K], v);
         rsq = fma(v, v, rsq);
       }
     }
-    for (int e = threadIdx.x; e < k * k; e += blockDim.x) bsq = fma(B[e], B[e], bsq);
+    double bsq = 0.0;
+    for (int e = threadIdx.x; e < K * K; e += blockDim.x) bsq = fma(B[e], B[e], bsq);
     rsq = block_sum(rsq, sc);
     bsq = block_sum(bsq, sc);
+    tstop(sc, kSiAY, tp);
     if (bsq > 0.0 && rsq <= 1e-26 * bsq) {
-      conv = true;
+      iters = it + 1;
       break;
     }
-    if (!(bsq > 0.0)) return false;
-    if (!cholqr_pass(W, rows, k, small, sc) || !cholqr_pass(W, rows, k, small, sc)) return false;
-    for (int64_t idx = threadIdx.x; idx < rows * k; idx += blockDim.x) U[idx] = W[idx];
+    if (!(bsq > 0.0)) return -1;
+    tp = tstart();
+    if (!cholqr_pass_k<K>(W, rows, small, sc) || !cholqr_pass_k<K>(W, rows, small, sc)) return -1;
+    for (int64_t idx = threadIdx.x; idx < rows * K; idx += blockDim.x) U[idx] = W[idx];
     __syncthreads();
+    tstop(sc, kSiQR, tp);
   }
-  if (!conv) return false;
+  const long long trr = tstart();
+  if (iters < 0) return -1;
   // Rayleigh-Ritz: U <- U R with B R = R diag(lambda), descending
   int* order = reinterpret_cast<int*>(misc);
   double* diag = nullptr;
-  const double* R = eig_run(B, k, small, order, dsm, &diag, sc);
+  const double* R = eig_run(B, K, small, order, dsm, &diag, sc);
   for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
-    double u[kSiMaxK];
+    double u[K];
 #pragma unroll
-    for (int l = 0; l < kSiMaxK; ++l) u[l] = l < k ? U[i + l * rows] : 0.0;
-    for (int j = 0; j < k; ++j) {
-      const double* rj = R + int64_t(order[j]) * k;
+    for (int l = 0; l < K; ++l) u[l] = U[i + l * rows];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const double* rj = R + int64_t(order[j]) * K;
       double v = 0.0;
 #pragma unroll
-      for (int l = 0; l < kSiMaxK; ++l)
-        if (l < k) v = fma(u[l], rj[l], v);
+      for (int l = 0; l < K; ++l) v = fma(u[l], rj[l], v);
       W[i + j * rows] = v;
     }
   }
   __syncthreads();
-  for (int64_t idx = threadIdx.x; idx < rows * k; idx += blockDim.x) U[idx] = W[idx];
+  for (int64_t idx = threadIdx.x; idx < rows * K; idx += blockDim.x) U[idx] = W[idx];
   __syncthreads();
-  sign_fix(U, rows, k, rows, nullptr, sc);
-  return true;
+  sign_fix(U, rows, K, rows, nullptr, sc);
+  tstop(sc, kSiRR, trr);
+  return iters;
+}
+
+__device__ bool llsv_subspace(const double* P, int64_t outer, int64_t rows, int64_t inner, int k, int kprev, double* U,
+                              double* si, double* dsm, double* misc, BlockScratch& sc) {
+  int it = -1;
+  switch (k) {
+#define TT_CASE(N) \
+  case N:          \
+    it = llsv_subspace_k<N>(P, outer, rows, inner, kprev, U, si, dsm, misc, sc); \
+    break;
+    TT_CASE(1) TT_CASE(2) TT_CASE(3) TT_CASE(4) TT_CASE(5) TT_CASE(6) TT_CASE(7) TT_CASE(8)
+    TT_CASE(9) TT_CASE(10) TT_CASE(11) TT_CASE(12) TT_CASE(13) TT_CASE(14) TT_CASE(15) TT_CASE(16)
+#undef TT_CASE
+    default:
+      break;
+  }
+  if (threadIdx.x == 0 && it > 0) sc.si_iters += it;
+  return it > 0;
 }
 
 // leading_left_singular_vectors (linalg.cpp:45-64) of the mode unfolding of a
@@ -386,12 +573,19 @@ __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows, int64_
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads, 2) leaf_als_kernel(Params prm, const LeafDesc* __restrict__ descs) {
   __shared__ BlockScratch sc;
-  extern __shared__ double dsm[];
+  __shared__ Pipe pipe;
+  extern __shared__ __align__(128) double dsm[];
   const long long t_kernel = tstart();
   if (threadIdx.x == 0) {
-    sc.eig_calls = sc.eig_sweeps = sc.si_ok = sc.si_fail = 0;
-    for (int i = 0; i < 8; ++i) sc.cyc[i] = 0;
+    sc.eig_calls = sc.eig_sweeps = sc.si_ok = sc.si_fail = sc.si_iters = 0;
+    for (int i = 0; i < 12; ++i) sc.cyc[i] = 0;
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&pipe.full[i], 1);
+      pipe.uses[i] = 0;
+    }
+    mbar_fence_init();
   }
+  __syncthreads();
   const LeafDesc D = descs[blockIdx.x];
   const int p = prm.p;
   int64_t d[kMaxP], rc[kMaxP], k[kMaxP];
@@ -406,74 +600,96 @@ __global__ void __launch_bounds__(kThreads, 2) leaf_als_kernel(Params prm, const
   double* misc = D.ws + lay.misc;
   const double* X = D.x;
   const int64_t ns = prod_range(d, 1, p);
-  const double norm_sq = bsumsq(X, D.len * ns, sc);
   for (int n = 0; n < p; ++n) {
     bcopy(D.out_f[n], D.init[n], d[n] * rc[n]);
     k[n] = rc[n];
   }
   int sweeps = 0, converged = 0;
-  if (norm_sq == 0.0) {  // tucker.cpp:96-100
-    bzero(D.out_core, prod_range(rc, 0, p));
-    converged = 1;
-  } else {
-    const double norm = sqrt(norm_sq);
-    double prev_fit = nan("");
-    for (int sweep = 0; sweep < prm.max_iters; ++sweep) {
-      // ---- mode 0: Y = X x_1 U_1^T ... x_{p-1} U_{p-1}^T, U_0 = llsv(M_0(Y))
-      const int64_t k0n = leaf_mode_rank(p, d, k, 0);
-      int64_t cur[kMaxP];
-      for (int m = 0; m < p; ++m) cur[m] = d[m];
-      const double* src = X;
-      int tog = 0;
-      for (int m = 1; m < p; ++m) {
-        double* dst = B[tog];
-        mode_product(src, prod_range(cur, 0, m), cur[m], prod_range(cur, m + 1, p), D.out_f[m], d[m], 1, k[m], dst,
-                     false, sc, m == 1 ? kPhBig : kPhTtm);
-        cur[m] = k[m];
-        src = dst;
-        tog ^= 1;
+  double norm_sq = 0.0, norm = 0.0;
+  double prev_fit = nan("");
+  for (int sweep = 0; sweep < prm.max_iters; ++sweep) {
+    // ---- mode 0: Y = X x_1 U_1^T ... x_{p-1} U_{p-1}^T, U_0 = llsv(M_0(Y))
+    const int64_t k0n = leaf_mode_rank(p, d, k, 0);
+    int64_t cur[kMaxP];
+    for (int m = 0; m < p; ++m) cur[m] = d[m];
+    const double* src = X;
+    int tog = 0;
+    for (int m = 1; m < p; ++m) {
+      double* dst = B[tog];
+      const int64_t inner = prod_range(cur, m + 1, p);
+      if (m == 1 && stream_ok(X, inner, int(k[1]))) {
+        // first contraction streams X through the TMA ring; sweep 0 also
+        // accumulates ||X||^2 (tucker.cpp:96)
+        const long long tb = tstart();
+        double nacc = 0.0;
+        ttm_stream(X, d[0], d[1], inner, D.out_f[1], int(k[1]), dst, dsm, pipe, sweep == 0 ? &nacc : nullptr,
+                   D.tmaps, 3);
+        if (sweep == 0) norm_sq = block_sum(nacc, sc);
+        tstop(sc, kPhBig, tb);
+      } else {
+        if (m == 1 && sweep == 0) norm_sq = bsumsq(X, D.len * ns, sc);
+        mode_product(src, prod_range(cur, 0, m), cur[m], inner, D.out_f[m], d[m], 1, k[m], dst, false, sc,
+                     m == 1 ? kPhBig : kPhTtm);
       }
-      llsv_unfold(src, 1, d[0], prod_range(cur, 1, p), k0n, D.out_f[0], G, V, misc, dsm, sc, k[0], D.ws + lay.SI);
-      k[0] = k0n;
-      // ---- W = X x_0 U_0^T : (k0, D_1, ..., D_{p-1})
-      mode_product(X, 1, d[0], ns, D.out_f[0], d[0], 1, k[0], W, false, sc, kPhBig);
-      // ---- modes n >= 1 from W
-      const double* Pn = W;
-      int64_t pc[kMaxP];
-      for (int n = 1; n < p; ++n) {
-        const int64_t kn = leaf_mode_rank(p, d, k, n);
-        pc[0] = k[0];
-        for (int m = 1; m < p; ++m) pc[m] = d[m];
-        const double* s2 = W;
-        int t2 = 0;
-        for (int m = 1; m < p; ++m) {
-          if (m == n) continue;
-          double* dst = B[t2];
-          mode_product(s2, prod_range(pc, 0, m), pc[m], prod_range(pc, m + 1, p), D.out_f[m], d[m], 1, k[m], dst,
-                       false, sc);
-          pc[m] = k[m];
-          s2 = dst;
-          t2 ^= 1;
-        }
-        llsv_unfold(s2, prod_range(pc, 0, n), d[n], prod_range(pc, n + 1, p), kn, D.out_f[n], G, V, misc, dsm, sc,
-                    k[n], D.ws + lay.SI);
-        k[n] = kn;
-        Pn = s2;
-      }
-      // ---- core = P_{p-1} x_{p-1} U_{p-1}^T  (== core_of(x, U), tucker.cpp:67-76)
-      mode_product(Pn, prod_range(k, 0, p - 1), d[p - 1], 1, D.out_f[p - 1], d[p - 1], 1, k[p - 1], D.out_core,
-                   false, sc);
-      const double core_sq = bsumsq(D.out_core, prod_range(k, 0, p), sc);
-      const double res = fmax(0.0, norm_sq - core_sq);
-      if (threadIdx.x == 0) D.objective[sweep] = res;
-      sweeps = sweep + 1;
-      const double fit = 1.0 - sqrt(res) / norm;
-      if (sweep > 0 && fabs(fit - prev_fit) < prm.tol) {
+      cur[m] = k[m];
+      src = dst;
+      tog ^= 1;
+    }
+    if (sweep == 0) {
+      if (norm_sq == 0.0) {  // tucker.cpp:96-100: init factors, zero core
+        bzero(D.out_core, prod_range(rc, 0, p));
         converged = 1;
         break;
       }
-      prev_fit = fit;
+      norm = sqrt(norm_sq);
     }
+    llsv_unfold(src, 1, d[0], prod_range(cur, 1, p), k0n, D.out_f[0], G, V, misc, dsm, sc, k[0], D.ws + lay.SI);
+    k[0] = k0n;
+    // ---- W = X x_0 U_0^T : (k0, D_1, ..., D_{p-1})
+    if (stream_ok(X, ns, int(k[0]))) {
+      const long long tb = tstart();
+      ttm_stream(X, 1, d[0], ns, D.out_f[0], int(k[0]), W, dsm, pipe, nullptr,
+                 D.tmaps ? static_cast<const char*>(D.tmaps) + 128 : nullptr, 2);
+      tstop(sc, kPhBig, tb);
+    } else {
+      mode_product(X, 1, d[0], ns, D.out_f[0], d[0], 1, k[0], W, false, sc, kPhBig);
+    }
+    // ---- modes n >= 1 from W
+    const double* Pn = W;
+    int64_t pc[kMaxP];
+    for (int n = 1; n < p; ++n) {
+      const int64_t kn = leaf_mode_rank(p, d, k, n);
+      pc[0] = k[0];
+      for (int m = 1; m < p; ++m) pc[m] = d[m];
+      const double* s2 = W;
+      int t2 = 0;
+      for (int m = 1; m < p; ++m) {
+        if (m == n) continue;
+        double* dst = B[t2];
+        mode_product(s2, prod_range(pc, 0, m), pc[m], prod_range(pc, m + 1, p), D.out_f[m], d[m], 1, k[m], dst,
+                     false, sc);
+        pc[m] = k[m];
+        s2 = dst;
+        t2 ^= 1;
+      }
+      llsv_unfold(s2, prod_range(pc, 0, n), d[n], prod_range(pc, n + 1, p), kn, D.out_f[n], G, V, misc, dsm, sc,
+                  k[n], D.ws + lay.SI);
+      k[n] = kn;
+      Pn = s2;
+    }
+    // ---- core = P_{p-1} x_{p-1} U_{p-1}^T  (== core_of(x, U), tucker.cpp:67-76)
+    mode_product(Pn, prod_range(k, 0, p - 1), d[p - 1], 1, D.out_f[p - 1], d[p - 1], 1, k[p - 1], D.out_core,
+                 false, sc);
+    const double core_sq = bsumsq(D.out_core, prod_range(k, 0, p), sc);
+    const double res = fmax(0.0, norm_sq - core_sq);
+    if (threadIdx.x == 0) D.objective[sweep] = res;
+    sweeps = sweep + 1;
+    const double fit = 1.0 - sqrt(res) / norm;
+    if (sweep > 0 && fabs(fit - prev_fit) < prm.tol) {
+      converged = 1;
+      break;
+    }
+    prev_fit = fit;
   }
   if (threadIdx.x == 0) {
     D.status[0] = sweeps;
@@ -491,6 +707,136 @@ __global__ void __launch_bounds__(kThreads, 2) leaf_als_kernel(Params prm, const
     for (int i = 0; i < 8; ++i) D.status[6 + kMaxP + i] = int(sc.cyc[i] >> 10);
     D.status[14 + kMaxP] = sc.si_ok;
     D.status[15 + kMaxP] = sc.si_fail;
+    D.status[16 + kMaxP] = sc.si_iters;
+    for (int i = 0; i < 4; ++i) D.status[17 + kMaxP + i] = int(sc.cyc[8 + i] >> 10);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// U_0 = blockdiag(V_sub,i) [E_i]  (L x K0, ld L), sign-fixed (linalg.cpp:15-31).
+// Pass 0 evaluates the rows without storing and finds each column's first
+// max-|.| row; pass 1 recomputes and stores U_0 once with the signs applied.
+// Two rows per thread are in flight, E_i is staged in shared memory.
+template <int K0>
+__device__ __noinline__ void materialize_u0_k(const StitchPart* __restrict__ parts, int s, const double* Ebase,
+                                              int64_t e_stride, double* __restrict__ U0, int64_t L, int* flips,
+                                              int64_t* idxbuf, double* Es, BlockScratch& sc) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int nt = int(blockDim.x);
+  for (int pass = 0; pass < 2; ++pass) {
+    double best[K0], sg[K0];
+    int64_t bidx[K0];
+#pragma unroll
+    for (int c = 0; c < K0; ++c) {
+      best[c] = -1.0;
+      bidx[c] = 0;
+      sg[c] = (pass == 1 && flips[c]) ? -1.0 : 1.0;
+    }
+    int64_t off = 0;
+    for (int i = 0; i < s; ++i) {
+      const int64_t r0 = parts[i].rho[0], len = parts[i].len, ld = parts[i].ld0;
+      const double* vs = parts[i].v0 + parts[i].row0;
+      const double* E = Ebase + int64_t(i) * e_stride;
+      __syncthreads();
+      for (int64_t e = threadIdx.x; e < r0 * K0; e += nt) Es[e] = E[e];
+      __syncthreads();
+      for (int64_t rb = threadIdx.x; rb < len; rb += 2 * nt) {
+        const int64_t ra = rb, rc = rb + nt;
+        const bool has_c = rc < len;
+        double oa[K0], ob[K0];
+#pragma unroll
+        for (int c = 0; c < K0; ++c) oa[c] = ob[c] = 0.0;
+        for (int64_t a = 0; a < r0; ++a) {
+          const double va = vs[ra + a * ld];
+          const double vb = has_c ? vs[rc + a * ld] : 0.0;
+#pragma unroll
+          for (int c = 0; c < K0; ++c) {
+            const double ev = Es[a + c * r0];
+            oa[c] = fma(va, ev, oa[c]);
+            ob[c] = fma(vb, ev, ob[c]);
+          }
+        }
+        if (pass == 1) {
+#pragma unroll
+          for (int c = 0; c < K0; ++c) {
+            U0[off + ra + c * L] = sg[c] * oa[c];
+            if (has_c) U0[off + rc + c * L] = sg[c] * ob[c];
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < K0; ++c) {
+            const double ma = fabs(oa[c]);
+            if (ma > best[c]) {
+              best[c] = ma;
+              bidx[c] = off + ra;
+              sg[c] = oa[c];
+            }
+            const double mb = has_c ? fabs(ob[c]) : -1.0;
+            if (mb > best[c]) {  // rc > ra: a tie keeps the earlier row
+              best[c] = mb;
+              bidx[c] = off + rc;
+              sg[c] = ob[c];
+            }
+          }
+        }
+      }
+      off += len;
+    }
+    if (pass == 0) {
+#pragma unroll
+      for (int c = 0; c < K0; ++c) {
+        double b = best[c], v = sg[c];
+        int64_t bi = bidx[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, b, o);
+          const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+          if (ob > b || (ob == b && oi < bi)) {
+            b = ob;
+            bi = oi;
+            v = ov;
+          }
+        }
+        if (l == 0) {
+          sc.red[w * kMaxVec + c] = b;
+          idxbuf[w * kMaxVec + c] = v < 0.0 ? -(bi + 1) : (bi + 1);
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x < K0) {
+        const int c = threadIdx.x;
+        double b = sc.red[c];
+        int64_t bi = idxbuf[c];
+        for (int ww = 1; ww < kWarps; ++ww) {
+          const double ob = sc.red[ww * kMaxVec + c];
+          const int64_t oi = idxbuf[ww * kMaxVec + c];
+          const int64_t ai = bi < 0 ? -bi : bi, ao = oi < 0 ? -oi : oi;
+          if (ob > b || (ob == b && ao < ai)) {
+            b = ob;
+            bi = oi;
+          }
+        }
+        flips[c] = bi < 0;
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+}
+
+__device__ bool materialize_u0(int k0, const StitchPart* parts, int s, const double* Ebase, int64_t e_stride,
+                               double* U0, int64_t L, int* flips, int64_t* idxbuf, double* Es, BlockScratch& sc) {
+  switch (k0) {
+#define TT_CASE(N) \
+  case N:          \
+    materialize_u0_k<N>(parts, s, Ebase, e_stride, U0, L, flips, idxbuf, Es, sc); \
+    return true;
+    TT_CASE(1) TT_CASE(2) TT_CASE(3) TT_CASE(4) TT_CASE(5) TT_CASE(6) TT_CASE(7) TT_CASE(8)
+    TT_CASE(9) TT_CASE(10) TT_CASE(11) TT_CASE(12) TT_CASE(13) TT_CASE(14) TT_CASE(15) TT_CASE(16)
+#undef TT_CASE
+    default:
+      return false;
   }
 }
 
@@ -527,8 +873,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   extern __shared__ double dsm[];
   const long long t_kernel = tstart();
   if (threadIdx.x == 0) {
-    sc.eig_calls = sc.eig_sweeps = sc.si_ok = sc.si_fail = 0;
-    for (int i = 0; i < 8; ++i) sc.cyc[i] = 0;
+    sc.eig_calls = sc.eig_sweeps = sc.si_ok = sc.si_fail = sc.si_iters = 0;
+    for (int i = 0; i < 12; ++i) sc.cyc[i] = 0;
   }
   const StitchDesc D = descs[blockIdx.x];
   const StitchPart* parts = parts_all + D.part0;
@@ -631,7 +977,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       if (k0n <= kSiMaxK && Q >= 2 * k0n && Q * k0n <= kSiMaxYK && rho0_sum >= k0n) {
         const long long t_si = tstart();
         double* Y = wk;                          // Q x k0
-        double* small = ws + lay.SI;             // 4 k x k
+        double* small = dsm + 4096 + kSiMaxYK;   // 4 k x k (shared memory)
         double* B = small + 4 * k0n * k0n;       // k x k
         const int kk = int(k0n);
         auto apply_S = [&](int i, const double* X, double* out) {  // out = S_i X (rho0 x k)
@@ -762,6 +1108,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           }
           if (rsq <= 1e-26 * bsq) {
             conv = true;
+            if (threadIdx.x == 0) sc.si_iters += it + 1;
             break;
           }
           for (int i = 0; i < s; ++i) bcopy(Ep(i), E2p(i), parts[i].rho[0] * kk);
@@ -931,91 +1278,94 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int64_t k0 = k[0];
     double* U0 = D.out_f[0];
     const long long tu = tstart();
-    // Row-parallel materialisation in column chunks of KU: each thread owns
-    // rows, keeps the first max-|.| row per column (sign convention), then a
-    // block argmax picks each column's sign. Rows of part i: Vsub_i[r,:] E_i.
-    constexpr int KU = 8;
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    for (int c0 = 0; c0 < k0; c0 += KU) {
-      const int nc = int(imin(KU, k0 - c0));
-      double best[KU];
-      int64_t bidx[KU];
-#pragma unroll
-      for (int c = 0; c < KU; ++c) {
-        best[c] = -1.0;
-        bidx[c] = 0;
-      }
-      int64_t off = 0;
-      for (int i = 0; i < s; ++i) {
-        const PartView pv = load_part(parts[i]);
-        const int64_t r0 = pv.rho[0];
-        const double* vs = pv.v0 + pv.row0;
-        const double* E = Ep(i) + c0 * r0;
-        for (int64_t r = threadIdx.x; r < pv.len; r += blockDim.x) {
-          double out[KU];
-#pragma unroll
-          for (int c = 0; c < KU; ++c) out[c] = 0.0;
-          for (int64_t a = 0; a < r0; ++a) {
-            const double v = vs[r + a * pv.ld0];
-#pragma unroll
-            for (int c = 0; c < KU; ++c)
-              if (c < nc) out[c] = fma(v, E[a + c * r0], out[c]);
-          }
-#pragma unroll
-          for (int c = 0; c < KU; ++c)
-            if (c < nc) {
-              U0[off + r + (c0 + c) * D.L] = out[c];
-              const double m = fabs(out[c]);
-              if (m > best[c]) {
-                best[c] = m;
-                bidx[c] = off + r;
-              }
+    if (any_zero_sigma ||
+        !materialize_u0(int(k0), parts, s, ws + lay.E, lay.per_part_E, U0, D.L, flips, idxbuf, dsm, sc)) {
+      // Row-parallel materialisation in column chunks of KU: each thread owns
+      // rows, keeps the first max-|.| row per column (sign convention), then a
+      // block argmax picks each column's sign. Rows of part i: Vsub_i[r,:] E_i.
+      constexpr int KU = 8;
+      const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+      for (int c0 = 0; c0 < k0; c0 += KU) {
+        const int nc = int(imin(KU, k0 - c0));
+        double best[KU];
+        int64_t bidx[KU];
+  #pragma unroll
+        for (int c = 0; c < KU; ++c) {
+          best[c] = -1.0;
+          bidx[c] = 0;
+        }
+        int64_t off = 0;
+        for (int i = 0; i < s; ++i) {
+          const PartView pv = load_part(parts[i]);
+          const int64_t r0 = pv.rho[0];
+          const double* vs = pv.v0 + pv.row0;
+          const double* E = Ep(i) + c0 * r0;
+          for (int64_t r = threadIdx.x; r < pv.len; r += blockDim.x) {
+            double out[KU];
+  #pragma unroll
+            for (int c = 0; c < KU; ++c) out[c] = 0.0;
+            for (int64_t a = 0; a < r0; ++a) {
+              const double v = vs[r + a * pv.ld0];
+  #pragma unroll
+              for (int c = 0; c < KU; ++c)
+                if (c < nc) out[c] = fma(v, E[a + c * r0], out[c]);
             }
+  #pragma unroll
+            for (int c = 0; c < KU; ++c)
+              if (c < nc) {
+                U0[off + r + (c0 + c) * D.L] = out[c];
+                const double m = fabs(out[c]);
+                if (m > best[c]) {
+                  best[c] = m;
+                  bidx[c] = off + r;
+                }
+              }
+          }
+          off += pv.len;
         }
-        off += pv.len;
-      }
-#pragma unroll
-      for (int c = 0; c < KU; ++c) {
-        double b = best[c];
-        int64_t bi = bidx[c];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ob = __shfl_xor_sync(0xffffffffu, b, o);
-          const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ob > b || (ob == b && oi < bi)) {
-            b = ob;
-            bi = oi;
+  #pragma unroll
+        for (int c = 0; c < KU; ++c) {
+          double b = best[c];
+          int64_t bi = bidx[c];
+  #pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, b, o);
+            const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ob > b || (ob == b && oi < bi)) {
+              b = ob;
+              bi = oi;
+            }
+          }
+          if (l == 0 && c < nc) {
+            sc.red[w * kMaxVec + c0 + c] = b;
+            idxbuf[w * kMaxVec + c0 + c] = bi;
           }
         }
-        if (l == 0 && c < nc) {
-          sc.red[w * kMaxVec + c0 + c] = b;
-          idxbuf[w * kMaxVec + c0 + c] = bi;
-        }
       }
-    }
-    __syncthreads();
-    if (any_zero_sigma) {
-      orthonormalize(U0, D.L, 0, int(k0), D.L, sc);
-      sign_fix(U0, D.L, int(k0), D.L, flips, sc);
-    } else {
-      if (threadIdx.x < k0) {
-        const int c = threadIdx.x;
-        double b = sc.red[c];
-        int64_t bi = idxbuf[c];
-        for (int ww = 1; ww < kWarps; ++ww) {
-          const double ob = sc.red[ww * kMaxVec + c];
-          const int64_t oi = idxbuf[ww * kMaxVec + c];
-          if (ob > b || (ob == b && oi < bi)) {
-            b = ob;
-            bi = oi;
+      __syncthreads();
+      if (any_zero_sigma) {
+        orthonormalize(U0, D.L, 0, int(k0), D.L, sc);
+        sign_fix(U0, D.L, int(k0), D.L, flips, sc);
+      } else {
+        if (threadIdx.x < k0) {
+          const int c = threadIdx.x;
+          double b = sc.red[c];
+          int64_t bi = idxbuf[c];
+          for (int ww = 1; ww < kWarps; ++ww) {
+            const double ob = sc.red[ww * kMaxVec + c];
+            const int64_t oi = idxbuf[ww * kMaxVec + c];
+            if (ob > b || (ob == b && oi < bi)) {
+              b = ob;
+              bi = oi;
+            }
           }
+          flips[c] = U0[bi + c * D.L] < 0.0;
         }
-        flips[c] = U0[bi + c * D.L] < 0.0;
+        __syncthreads();
+        for (int64_t idx = threadIdx.x; idx < D.L * k0; idx += blockDim.x)
+          if (flips[idx / D.L]) U0[idx] = -U0[idx];
+        __syncthreads();
       }
-      __syncthreads();
-      for (int64_t idx = threadIdx.x; idx < D.L * k0; idx += blockDim.x)
-        if (flips[idx / D.L]) U0[idx] = -U0[idx];
-      __syncthreads();
     }
     const int64_t slice = prod_range(k, 1, p);
     for (int64_t e = threadIdx.x; e < k0 * slice; e += blockDim.x)
@@ -1039,6 +1389,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int i = 0; i < 8; ++i) D.status[6 + kMaxP + i] = int(sc.cyc[i] >> 10);
     D.status[14 + kMaxP] = sc.si_ok;
     D.status[15 + kMaxP] = sc.si_fail;
+    D.status[16 + kMaxP] = sc.si_iters;
+    for (int i = 0; i < 4; ++i) D.status[17 + kMaxP + i] = int(sc.cyc[8 + i] >> 10);
   }
 }
 
@@ -1049,10 +1401,10 @@ cudaError_t launch_leaf(const Params& prm, const LeafDesc* d_descs, int n, cudaS
   if (n <= 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(leaf_als_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDynSmem));
+    cudaFuncSetAttribute(leaf_als_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kLeafDynSmem));
     attr = true;
   }
-  leaf_als_kernel<<<n, kThreads, kDynSmem, st>>>(prm, d_descs);
+  leaf_als_kernel<<<n, kThreads, kLeafDynSmem, st>>>(prm, d_descs);
   g_launches.fetch_add(1);
   return cudaGetLastError();
 }

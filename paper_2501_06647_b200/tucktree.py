@@ -439,8 +439,12 @@ def kernel_launches() -> int:
 
 def solver_stats() -> dict:
     """Cumulative ALS/eigensolver counters (problems, ALS sweeps, eig calls, Jacobi sweeps)."""
-    out = np.zeros(14, dtype=np.int64)
+    out = np.zeros(38, dtype=np.int64)
     lib().tt_solver_stats(out.ctypes.data_as(i64ptr))
-    return dict(zip(("problems", "als_sweeps", "eig_calls", "jacobi_sweeps", "kcyc_eig", "kcyc_gram", "kcyc_ttm",
-                     "kcyc_gemm", "kcyc_ortho_sign", "kcyc_u0", "kcyc_leaf_x", "kcyc_problem", "subspace_ok",
-                     "subspace_fallback"), (int(v) for v in out)))
+    names = ("problems", "als_sweeps", "eig_calls", "jacobi_sweeps", "kcyc_eig", "kcyc_gram", "kcyc_ttm", "kcyc_gemm",
+             "kcyc_ortho_sign", "kcyc_u0", "kcyc_leaf_x", "kcyc_problem", "subspace_ok", "subspace_fallback",
+             "subspace_iters", "kcyc_si_atu", "kcyc_si_ay", "kcyc_si_qr", "kcyc_si_rr")
+    d = {n: int(out[i]) + int(out[19 + i]) for i, n in enumerate(names)}
+    d["leaf"] = {n: int(out[i]) for i, n in enumerate(names)}
+    d["stitch"] = {n: int(out[19 + i]) for i, n in enumerate(names)}
+    return d
