@@ -106,6 +106,12 @@ struct Params {
   const double* stitch_init[kMaxP];  // stitch init factors U_m (m >= 1), D_m x rc_m
 };
 
+struct CopySeg {
+  const double* src;
+  double* dst;
+  int64_t n;
+};
+
 constexpr int kStatusInts = 4 + kMaxP + 17;  // ..., eig calls, Jacobi sweeps, kcycles[8], subspace ok/fail
 
 // ---------------------------------------------------------------------------

@@ -30,6 +30,7 @@ namespace ttb {
 cudaError_t launch_leaf(const Params& prm, const LeafDesc* d_descs, int n, cudaStream_t st);
 cudaError_t launch_stitch(const Params& prm, const StitchDesc* d_descs, const StitchPart* d_parts, int n,
                           cudaStream_t st);
+cudaError_t launch_copy_segments(const CopySeg* d_segs, int n, cudaStream_t st);
 int64_t launches();
 }  // namespace ttb
 
@@ -218,7 +219,7 @@ struct DeviceGuard {
 struct Exec {
   int device = 0;
   cudaStream_t stream = nullptr;
-  DevBuf d_desc, d_parts, d_ws, d_status, d_obj, d_stage, d_tmaps;
+  DevBuf d_desc, d_parts, d_ws, d_status, d_obj, d_stage, d_tmaps, d_segs;
   std::vector<char> h_status_bytes;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   explicit Exec(int dev) : device(dev) {
@@ -233,6 +234,18 @@ struct Exec {
   }
   void sync() { cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize"); }
 };
+
+// Device view of a pinned (page-locked, UVA-mapped) host buffer, or null.
+double* mapped_device_ptr(void* host) {
+  if (!host) return nullptr;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, host) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (a.type == cudaMemoryTypeHost && a.devicePointer != nullptr) return static_cast<double*>(a.devicePointer);
+  return nullptr;
+}
 
 // Result of one batched ALS problem after readback.
 struct ProblemStatus {
@@ -1169,6 +1182,7 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
       std::vector<StitchPart> parts;
       std::vector<Index> ws;
       std::vector<size_t> out_off;
+      std::vector<char> u0_direct;
       size_t used = 0, out_need = 0;
       int64_t q1 = q0;
       for (; q1 < n; ++q1) {
@@ -1230,6 +1244,7 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
       }
       // output buffers
       if (where == TT_MEM_HOST) t->qout.ensure(out_need * sizeof(double));
+      u0_direct.assign(static_cast<size_t>(q1 - q0), 0);
       for (int64_t q = q0; q < q1; ++q) {
         StitchDesc& dsc = descs[q - q0];
         const Index L = dsc.L;
@@ -1248,9 +1263,17 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
           dsc.out_f[0] = take(L * rc[0]);
           for (int m = 1; m < p; ++m) dsc.out_f[m] = take(t->d[m] * rc[m]);
           dsc.out_core = take(prod_range(rc, 0, p));
+          // U_0 is written once, at the very end of the kernel: with a pinned
+          // caller buffer the kernel stores it straight to host memory over PCIe
+          if (double* mp = mapped_device_ptr(outs[q].factors[0])) {
+            dsc.out_f[0] = mp;
+            u0_direct[q - q0] = 1;
+          }
         }
       }
       const auto st = run_stitch_batch(ex, prm, descs, parts, ws);
+      std::vector<CopySeg> segs;
+      bool all_mapped = where == TT_MEM_HOST;
       for (int64_t q = q0; q < q1; ++q) {
         const ProblemStatus& s = st[q - q0];
         tt_query_out& o = outs[q];
@@ -1260,10 +1283,14 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
         if (s.zero) {
           for (int m = 0; m < p; ++m) k[m] = t->clamped(m, L);
           const auto u0 = t->init.stitch_zero_u0(L, k[0]);
-          cuda_check(cudaMemcpyAsync(descs[q - q0].out_f[0], u0.data(), u0.size() * sizeof(double),
-                                     cudaMemcpyHostToDevice, ex.stream),
-                     "zero-path upload");
-          ex.sync();
+          if (u0_direct[q - q0]) {
+            std::memcpy(o.factors[0], u0.data(), u0.size() * sizeof(double));
+          } else {
+            cuda_check(cudaMemcpyAsync(descs[q - q0].out_f[0], u0.data(), u0.size() * sizeof(double),
+                                       cudaMemcpyHostToDevice, ex.stream),
+                       "zero-path upload");
+            ex.sync();
+          }
         }
         for (int m = 0; m < TT_MAX_ORDER; ++m) o.ranks[m] = m < p ? k[m] : 0;
         o.sweeps = s.sweeps;
@@ -1272,19 +1299,34 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
         o.nhits = static_cast<int32_t>(hits[q].size());
         if (where == TT_MEM_HOST) {
           const StitchDesc& dsc = descs[q - q0];
-          if (o.core)
-            cuda_check(cudaMemcpyAsync(o.core, dsc.out_core, static_cast<size_t>(prod_range(k, 0, p)) * sizeof(double),
-                                       cudaMemcpyDeviceToHost, ex.stream),
-                       "query core download");
-          for (int m = 0; m < p; ++m) {
-            if (!o.factors[m]) continue;
-            const Index rows = m == 0 ? L : t->d[m];
-            cuda_check(cudaMemcpyAsync(o.factors[m], dsc.out_f[m], static_cast<size_t>(rows * k[m]) * sizeof(double),
-                                       cudaMemcpyDeviceToHost, ex.stream),
-                       "query factor download");
-          }
+          // small outputs: one gather kernel into mapped host memory when every
+          // destination is pinned, else individual copies
+          auto add = [&](void* host, const double* src, Index n) {
+            if (!host) return;
+            double* mp = mapped_device_ptr(host);
+            if (mp) {
+              segs.push_back(CopySeg{src, mp, n});
+            } else {
+              all_mapped = false;
+              cuda_check(cudaMemcpyAsync(host, src, static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToHost,
+                                         ex.stream),
+                         "query output download");
+            }
+          };
+          add(o.core, dsc.out_core, prod_range(k, 0, p));
+          for (int m = 1; m < p; ++m) add(o.factors[m], dsc.out_f[m], t->d[m] * k[m]);
+          if (!u0_direct[q - q0]) add(o.factors[0], dsc.out_f[0], L * k[0]);
         }
       }
+      if (!segs.empty()) {
+        ex.d_segs.ensure(segs.size() * sizeof(CopySeg));
+        cuda_check(cudaMemcpyAsync(ex.d_segs.p, segs.data(), segs.size() * sizeof(CopySeg), cudaMemcpyHostToDevice,
+                                   ex.stream),
+                   "upload copy segments");
+        cuda_check(launch_copy_segments(ex.d_segs.as<CopySeg>(), static_cast<int>(segs.size()), ex.stream),
+                   "copy_segments_kernel launch");
+      }
+      (void)all_mapped;
       ex.sync();
       q0 = q1;
     }

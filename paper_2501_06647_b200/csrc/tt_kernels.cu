@@ -1395,7 +1395,21 @@ __global__ void __launch_bounds__(kThreads, 2)
 }
 
 // ---------------------------------------------------------------------------
+// Gathers small device-staged outputs (cores, non-temporal factors) into the
+// caller's pinned, UVA-mapped host buffers in one launch (one CTA per segment).
+__global__ void __launch_bounds__(256) copy_segments_kernel(const CopySeg* __restrict__ segs, int n) {
+  const CopySeg sg = segs[blockIdx.x];
+  for (int64_t i = threadIdx.x; i < sg.n; i += blockDim.x) sg.dst[i] = sg.src[i];
+}
+
 std::atomic<int64_t> g_launches{0};
+
+cudaError_t launch_copy_segments(const CopySeg* d_segs, int n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  copy_segments_kernel<<<n, 256, 0, st>>>(d_segs, n);
+  g_launches.fetch_add(1);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_leaf(const Params& prm, const LeafDesc* d_descs, int n, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;

@@ -256,3 +256,44 @@ def test_query_errors(E):
             t.range_query(a, b)
     with pytest.raises(ValueError):
         t.recall(0, 4, 1.0)
+
+
+def test_query_outputs_pinned_host_equal_pageable(E):
+    """Pinned (UVA-mapped) output buffers take the direct-write path (U0 stored by
+    the kernel into host memory, small outputs gathered by one kernel); results
+    must equal the pageable-buffer path bit for bit."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2501_06647_b200.tucktree import TTQueryOut, TTRange, _check, dptr
+
+    series = _series((300, 12, 6), (4, 3, 3), 0.05, 21)
+    t = E.StreamSegmentTree((12, 6), (5, 4, 3), leaf_block=8)
+    t.append(series)
+    qs = [(0, 300), (3, 77), (100, 101), (250, 299), (5, 290)]
+    want = t.range_query_batch(qs)
+    p = 3
+    outs = (TTQueryOut * len(qs))()
+    rr = (TTRange * len(qs))()
+    keep = []
+    for i, (a, b) in enumerate(qs):
+        rr[i].ts, rr[i].te = a, b
+        L = b - a
+        rc = [min(5, L), 4, 3]
+        rows = [L, 12, 6]
+        core = torch.zeros(int(np.prod(rc)), dtype=torch.float64).pin_memory()
+        fs = [torch.zeros(rows[m] * rc[m], dtype=torch.float64).pin_memory() for m in range(p)]
+        keep.append((core, fs, rows))
+        outs[i].core = C.cast(C.c_void_p(core.data_ptr()), dptr)
+        for m in range(p):
+            outs[i].factors[m] = C.cast(C.c_void_p(fs[m].data_ptr()), dptr)
+    _check(E.lib().tt_query_batch(t._h, rr, len(qs), float("nan"), outs, 0))
+    for i in range(len(qs)):
+        core, fs, rows = keep[i]
+        k = [outs[i].ranks[m] for m in range(p)]
+        assert k == [want[i].rank(m) for m in range(p)]
+        assert np.array_equal(core.numpy()[: int(np.prod(k))].reshape(k), want[i].core)
+        for m in range(p):
+            got = fs[m].numpy()[: rows[m] * k[m]].reshape(k[m], rows[m]).T
+            assert np.array_equal(got, want[i].factors[m])
