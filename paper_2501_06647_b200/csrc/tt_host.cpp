@@ -368,20 +368,34 @@ std::vector<ProblemStatus> run_leaf_batch(Exec& ex, const Params& prm, std::vect
   return st;
 }
 
-std::vector<ProblemStatus> run_stitch_batch(Exec& ex, const Params& prm, std::vector<StitchDesc>& descs,
+std::vector<ProblemStatus> run_stitch_batch(Exec& ex, const Params& prm, std::vector<StitchDesc>& descs_in,
                                             const std::vector<StitchPart>& parts, const std::vector<Index>& ws_sizes) {
-  const int n = static_cast<int>(descs.size());
+  const int n = static_cast<int>(descs_in.size());
+  std::vector<ProblemStatus> st_out(static_cast<size_t>(n));
+  if (n == 0) return st_out;
+  // Launch longest-first: CTAs are dispatched roughly in index order and query
+  // costs vary ~100x (L and the part count), so LPT order shrinks the tail.
+  std::vector<int> perm(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) perm[i] = i;
+  auto cost = [&](int i) { return double(descs_in[i].L) + 4096.0 * descs_in[i].nparts; };
+  std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return cost(a) > cost(b); });
+  std::vector<StitchDesc> descs(static_cast<size_t>(n));
+  std::vector<Index> wsz(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) {
+    descs[i] = descs_in[perm[i]];
+    wsz[i] = ws_sizes[perm[i]];
+  }
   std::vector<ProblemStatus> st(static_cast<size_t>(n));
-  if (n == 0) return st;
+  const std::vector<Index>& ws_sizes_p = wsz;
   size_t ws_total = 0;
-  for (Index w : ws_sizes) ws_total += static_cast<size_t>(w);
+  for (Index w : ws_sizes_p) ws_total += static_cast<size_t>(w);
   ex.d_ws.ensure(ws_total * sizeof(double));
   ex.d_status.ensure(size_t(n) * kStatusInts * sizeof(int32_t));
   ex.d_obj.ensure(size_t(n) * prm.max_iters * sizeof(double));
   size_t off = 0;
   for (int i = 0; i < n; ++i) {
     descs[i].ws = ex.d_ws.as<double>() + off;
-    off += static_cast<size_t>(ws_sizes[i]);
+    off += static_cast<size_t>(ws_sizes_p[i]);
     descs[i].status = ex.d_status.as<int32_t>() + size_t(i) * kStatusInts;
     descs[i].objective = ex.d_obj.as<double>() + size_t(i) * prm.max_iters;
   }
@@ -421,7 +435,13 @@ std::vector<ProblemStatus> run_stitch_batch(Exec& ex, const Params& prm, std::ve
     for (int q = 0; q < 4; ++q) g_stats[1][15 + q] += s[17 + kMaxP + q];
     st[i].objective.assign(ho.begin() + size_t(i) * prm.max_iters, ho.begin() + size_t(i) * prm.max_iters + s[0]);
   }
-  return st;
+  for (int i = 0; i < n; ++i) {
+    st_out[perm[i]] = std::move(st[i]);
+    descs_in[perm[i]].ws = descs[i].ws;
+    descs_in[perm[i]].status = descs[i].status;
+    descs_in[perm[i]].objective = descs[i].objective;
+  }
+  return st_out;
 }
 
 // Shared per-shape constants: leaf init factors per block length and the
