@@ -30,6 +30,7 @@ struct BlockScratch {
   int rotated[2];
   int eig_calls, eig_sweeps;  // instrumentation (Jacobi sweeps per problem)
   int si_ok, si_fail, si_iters;  // subspace-iteration outcomes and iterations
+  int dsm_cap;                   // doubles of dynamic shared memory in this launch
   long long cyc[12];          // instrumentation: cycles per phase (see kPh*, kSi*)
 };
 
@@ -61,7 +62,8 @@ __device__ __forceinline__ double block_sum(double v, BlockScratch& sc) {
   __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
-    for (int i = 0; i < kWarps; ++i) s += sc.red[i];
+    const int nw = int(blockDim.x >> 5);
+    for (int i = 0; i < nw; ++i) s += sc.red[i];
     sc.bcast[0] = s;
   }
   __syncthreads();
@@ -83,7 +85,8 @@ __device__ __forceinline__ void block_sum_vec(const double (&v)[NV], int nv, Blo
   __syncthreads();
   if (threadIdx.x < nv) {
     double s = 0.0;
-    for (int k = 0; k < kWarps; ++k) s += sc.red[k * kMaxVec + threadIdx.x];
+    const int nw = int(blockDim.x >> 5);
+    for (int k = 0; k < nw; ++k) s += sc.red[k * kMaxVec + threadIdx.x];
     sc.vec[threadIdx.x] = s;
   }
   __syncthreads();
@@ -329,7 +332,8 @@ __device__ int sym_eig(double* A, int n, double* V, int* order, BlockScratch& sc
   const int n2 = n + (n & 1);
   const int np = n2 / 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int j = warp; j < n; j += kWarps)
+  const int nwk = int(blockDim.x >> 5);
+  for (int j = warp; j < n; j += nwk)
     for (int i = lane; i < n; i += 32) V[i + j * n] = (i == j) ? 1.0 : 0.0;
   if (threadIdx.x < 2) sc.rotated[threadIdx.x] = 0;
   if (n <= 1) {
@@ -342,7 +346,7 @@ __device__ int sym_eig(double* A, int n, double* V, int* order, BlockScratch& sc
   // precision, the absolute floor stops the solver from chasing rounding noise
   // between numerically-zero eigenvalues (eigenvector error <= eps_a/gap).
   double fro = 0.0;
-  for (int j = warp; j < n; j += kWarps)
+  for (int j = warp; j < n; j += nwk)
     for (int i = lane; i < n; i += 32) fro = fma(A[i + j * n], A[i + j * n], fro);
   const double abs_thr = 1e-15 * sqrt(block_sum(fro, sc));
   const double eps2 = 1e-28;  // relative test (1e-14)^2
@@ -389,7 +393,7 @@ __device__ int sym_eig(double* A, int n, double* V, int* order, BlockScratch& sc
       }
       __syncthreads();
       // A <- J^T A J on 2x2 blocks (one owner thread per block), V <- V J.
-      for (int P2 = warp; P2 < np; P2 += kWarps) {
+      for (int P2 = warp; P2 < np; P2 += nwk) {
         const int p2 = sc.jp[P2], q2 = sc.jq[P2];
         const double c2 = sc.jc[P2], s2 = sc.js[P2];
         const bool hq2 = q2 < n;
@@ -423,7 +427,7 @@ __device__ int sym_eig(double* A, int n, double* V, int* order, BlockScratch& sc
           if (hq && hq2) A[q + q2 * n] = s2 * x10 + c2 * x11;
         }
       }
-      for (int P1 = warp; P1 < np; P1 += kWarps) {
+      for (int P1 = warp; P1 < np; P1 += nwk) {
         const double s1 = sc.js[P1];
         if (s1 == 0.0) continue;
         const int p = sc.jp[P1], q = sc.jq[P1];
@@ -523,10 +527,11 @@ __device__ int sym_eig_smem(double* S, int n, int* order, BlockScratch& sc) {
       }
       any |= __any_sync(0xffffffffu, sn != 0.0);
       // gather the pair parameters this warp needs up front (overlapped shuffles)
-      int p2v[4], q2v[4];
-      double c2v[4], s2v[4];
+      constexpr int PU = 8;  // pairs per warp (>= 4 warps for np <= 26)
+      int p2v[PU], q2v[PU];
+      double c2v[PU], s2v[PU];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < PU; ++u) {
         const int P2 = warp + u * nwarps;
         const int src = P2 < 32 ? P2 : 0;
         p2v[u] = __shfl_sync(0xffffffffu, p, src);
@@ -538,7 +543,7 @@ __device__ int sym_eig_smem(double* S, int n, int* order, BlockScratch& sc) {
       if (lane < np) {
         const bool hq = q < n;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < PU; ++u) {
           const int P2 = warp + u * nwarps;
           if (P2 >= np) break;
           const int p2 = p2v[u], q2 = q2v[u];
@@ -571,7 +576,7 @@ __device__ int sym_eig_smem(double* S, int n, int* order, BlockScratch& sc) {
       }
       // V = V J (warp <-> pair, lanes <-> rows); same pairs as the P2 set above
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < PU; ++u) {
         const int P1 = warp + u * nwarps;
         if (P1 >= np) break;
         const double s1 = s2v[u];
@@ -644,7 +649,7 @@ __device__ void sign_fix(double* U, int64_t rows, int k, int64_t ld, int* flips,
     if (threadIdx.x == 0) {
       double b = sc.red[0];
       int64_t idx = __double_as_longlong(sc.red[kWarps]);
-      for (int i = 1; i < kWarps; ++i) {
+      for (int i = 1; i < int(blockDim.x >> 5); ++i) {
         const double ob = sc.red[i];
         const int64_t oi = __double_as_longlong(sc.red[kWarps + i]);
         if (ob > b || (ob == b && oi < idx)) {

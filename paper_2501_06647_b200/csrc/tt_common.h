@@ -179,6 +179,7 @@ TT_HD StitchWs stitch_ws_layout(int p, int64_t L, const int64_t* d, const int64_
   const int64_t chain = prod_range(rcx, 0, p);
   int64_t z = 0;
   for (int n = 1; n < p; ++n) z = imax(z, prod_except(rc, p, n) * dd[n]);
+  z = imax(z, int64_t(nparts) * rcx[0] * rc[0]);  // Z doubles as the mode-0 residual scratch
   StitchWs w;
   w.gram_n = g;
   w.per_part_P = pp;
