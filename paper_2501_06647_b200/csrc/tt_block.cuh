@@ -62,8 +62,7 @@ __device__ __forceinline__ double block_sum(double v, BlockScratch& sc) {
   __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
-    const int nw = int(blockDim.x >> 5);
-    for (int i = 0; i < nw; ++i) s += sc.red[i];
+    for (int i = 0; i < kWarps; ++i) s += sc.red[i];
     sc.bcast[0] = s;
   }
   __syncthreads();
@@ -85,8 +84,7 @@ __device__ __forceinline__ void block_sum_vec(const double (&v)[NV], int nv, Blo
   __syncthreads();
   if (threadIdx.x < nv) {
     double s = 0.0;
-    const int nw = int(blockDim.x >> 5);
-    for (int k = 0; k < nw; ++k) s += sc.red[k * kMaxVec + threadIdx.x];
+    for (int k = 0; k < kWarps; ++k) s += sc.red[k * kMaxVec + threadIdx.x];
     sc.vec[threadIdx.x] = s;
   }
   __syncthreads();
@@ -332,7 +330,7 @@ __device__ int sym_eig(double* A, int n, double* V, int* order, BlockScratch& sc
   const int n2 = n + (n & 1);
   const int np = n2 / 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nwk = int(blockDim.x >> 5);
+  constexpr int nwk = kWarps;
   for (int j = warp; j < n; j += nwk)
     for (int i = lane; i < n; i += 32) V[i + j * n] = (i == j) ? 1.0 : 0.0;
   if (threadIdx.x < 2) sc.rotated[threadIdx.x] = 0;
@@ -527,7 +525,7 @@ __device__ int sym_eig_smem(double* S, int n, int* order, BlockScratch& sc) {
       }
       any |= __any_sync(0xffffffffu, sn != 0.0);
       // gather the pair parameters this warp needs up front (overlapped shuffles)
-      constexpr int PU = 8;  // pairs per warp (>= 4 warps for np <= 26)
+      constexpr int PU = 4;  // pairs per warp: needs >= 7 warps for np <= 26 (256-thread CTAs)
       int p2v[PU], q2v[PU];
       double c2v[PU], s2v[PU];
 #pragma unroll
@@ -649,7 +647,7 @@ __device__ void sign_fix(double* U, int64_t rows, int k, int64_t ld, int* flips,
     if (threadIdx.x == 0) {
       double b = sc.red[0];
       int64_t idx = __double_as_longlong(sc.red[kWarps]);
-      for (int i = 1; i < int(blockDim.x >> 5); ++i) {
+      for (int i = 1; i < kWarps; ++i) {
         const double ob = sc.red[i];
         const int64_t oi = __double_as_longlong(sc.red[kWarps + i]);
         if (ob > b || (ob == b && oi < idx)) {

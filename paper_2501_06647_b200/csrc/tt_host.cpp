@@ -221,18 +221,27 @@ struct Exec {
   cudaStream_t stream = nullptr;
   DevBuf d_desc, d_parts, d_ws, d_status, d_obj, d_stage, d_tmaps, d_segs;
   std::vector<char> h_status_bytes;
+  cudaStream_t copy = nullptr;  // device-to-host result downloads, overlapping later launches
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  static constexpr int kWaveEvents = 16;
+  cudaEvent_t wave_ev[kWaveEvents] = {};
   explicit Exec(int dev) : device(dev) {
     DeviceGuard g(dev);
     cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking), "cudaStreamCreate");
     for (auto& e : ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    for (auto& e : wave_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
   }
   ~Exec() {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    for (auto& e : wave_ev)
+      if (e) cudaEventDestroy(e);
+    if (copy) cudaStreamDestroy(copy);
     if (stream) cudaStreamDestroy(stream);
   }
   void sync() { cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize"); }
+  void sync_copy() { cuda_check(cudaStreamSynchronize(copy), "cudaStreamSynchronize"); }
 };
 
 // Device view of a pinned (page-locked, UVA-mapped) host buffer, or null.
@@ -539,7 +548,8 @@ struct tt_tree {
   DevBuf tail;  // B slices (device)
   InitCache init;
   DevBuf stage;  // host-burst staging
-  DevBuf qout;   // query output staging (host-destination batches)
+  DevBuf qout;      // query output staging (host-destination batches)
+  DevBuf qscratch;  // device scratch for outputs the caller did not request
   DevBuf tailq;  // tail-part scratch for queries
   double timing[3] = {0, 0, 0};
   mutable std::mutex qmu;
@@ -1202,7 +1212,6 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
       std::vector<StitchPart> parts;
       std::vector<Index> ws;
       std::vector<size_t> out_off;
-      std::vector<char> u0_direct;
       size_t used = 0, out_need = 0;
       int64_t q1 = q0;
       for (; q1 < n; ++q1) {
@@ -1263,35 +1272,196 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
         out_need += onum;
       }
       // output buffers
-      if (where == TT_MEM_HOST) t->qout.ensure(out_need * sizeof(double));
-      u0_direct.assign(static_cast<size_t>(q1 - q0), 0);
-      for (int64_t q = q0; q < q1; ++q) {
-        StitchDesc& dsc = descs[q - q0];
-        const Index L = dsc.L;
-        Index rc[kMaxP];
-        for (int m = 0; m < p; ++m) rc[m] = t->clamped(m, L);
-        if (where == TT_MEM_DEVICE) {
-          for (int m = 0; m < p; ++m) dsc.out_f[m] = outs[q].factors[m];
-          dsc.out_core = outs[q].core;
-        } else {
-          double* cur = t->qout.as<double>() + out_off[q - q0];
-          auto take = [&cur](Index nd) {
-            double* r = cur;
-            cur += (nd + 31) & ~Index(31);
-            return r;
+      const int64_t nc = q1 - q0;
+      // Pinned host outputs (the serving case) are DMA'd on the copy stream.
+      // Staging mirrors the caller's layout: outputs that are adjacent in host
+      // memory are adjacent in staging, so a wave's download is a few large
+      // copies. Every output is sized for the clamped requested ranks (the
+      // tt_query_out contract) and copied at that size.
+      struct OutRef {
+        char* host;
+        size_t bytes;
+        int64_t q;  // chunk-relative query
+        int m;      // -1 core, else factor mode
+      };
+      std::vector<OutRef> orefs;
+      bool dma = where == TT_MEM_HOST;
+      if (dma) {
+        for (int64_t q = q0; q < q1 && dma; ++q) {
+          const Index L = descs[q - q0].L;
+          Index rc[kMaxP];
+          for (int m = 0; m < p; ++m) rc[m] = t->clamped(m, L);
+          auto addr = [&](double* h, Index nd, int m) {
+            if (!h) return;
+            if (!mapped_device_ptr(h)) dma = false;
+            orefs.push_back(OutRef{reinterpret_cast<char*>(h), static_cast<size_t>(nd) * sizeof(double), q - q0, m});
           };
-          dsc.out_f[0] = take(L * rc[0]);
-          for (int m = 1; m < p; ++m) dsc.out_f[m] = take(t->d[m] * rc[m]);
-          dsc.out_core = take(prod_range(rc, 0, p));
-          // U_0 is written once, at the very end of the kernel: with a pinned
-          // caller buffer the kernel stores it straight to host memory over PCIe
-          if (double* mp = mapped_device_ptr(outs[q].factors[0])) {
-            dsc.out_f[0] = mp;
-            u0_direct[q - q0] = 1;
+          addr(outs[q].core, prod_range(rc, 0, p), -1);
+          addr(outs[q].factors[0], L * rc[0], 0);
+          for (int m = 1; m < p; ++m) addr(outs[q].factors[m], t->d[m] * rc[m], m);
+        }
+      }
+      std::vector<size_t> stage_off;  // per oref
+      if (dma) {
+        std::vector<size_t> idx(orefs.size());
+        for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
+        std::sort(idx.begin(), idx.end(), [&](size_t x, size_t y) { return orefs[x].host < orefs[y].host; });
+        for (size_t i = 1; i < idx.size(); ++i)
+          if (orefs[idx[i - 1]].host + orefs[idx[i - 1]].bytes > orefs[idx[i]].host)
+            fail(TT_EINVAL, "range_query: output buffers overlap");
+        stage_off.assign(orefs.size(), 0);
+        size_t off = 0;
+        for (size_t i = 0; i < idx.size(); ++i) {
+          // clusters of host-adjacent outputs are packed back to back
+          stage_off[idx[i]] = off;
+          off += (orefs[idx[i]].bytes + 7) & ~size_t(7);
+        }
+        t->qout.ensure(std::max<size_t>(off, 8));
+        for (size_t i = 0; i < orefs.size(); ++i) {
+          double* dptr = reinterpret_cast<double*>(t->qout.as<char>() + stage_off[i]);
+          StitchDesc& dsc = descs[orefs[i].q];
+          if (orefs[i].m < 0)
+            dsc.out_core = dptr;
+          else
+            dsc.out_f[orefs[i].m] = dptr;
+        }
+        // outputs the caller did not request still need device scratch
+        size_t extra = 0;
+        for (int64_t q = q0; q < q1; ++q) {
+          const Index L = descs[q - q0].L;
+          Index rc[kMaxP];
+          for (int m = 0; m < p; ++m) rc[m] = t->clamped(m, L);
+          if (!outs[q].core) extra += static_cast<size_t>(prod_range(rc, 0, p));
+          for (int m = 0; m < p; ++m)
+            if (!outs[q].factors[m]) extra += static_cast<size_t>((m == 0 ? L : t->d[m]) * rc[m]);
+        }
+        if (extra) {
+          t->qscratch.ensure(extra * sizeof(double));
+          double* cur = t->qscratch.as<double>();
+          for (int64_t q = q0; q < q1; ++q) {
+            const Index L = descs[q - q0].L;
+            Index rc[kMaxP];
+            for (int m = 0; m < p; ++m) rc[m] = t->clamped(m, L);
+            StitchDesc& dsc = descs[q - q0];
+            if (!outs[q].core) {
+              dsc.out_core = cur;
+              cur += prod_range(rc, 0, p);
+            }
+            for (int m = 0; m < p; ++m)
+              if (!outs[q].factors[m]) {
+                dsc.out_f[m] = cur;
+                cur += (m == 0 ? L : t->d[m]) * rc[m];
+              }
+          }
+        }
+      } else {
+        if (where == TT_MEM_HOST) t->qout.ensure(out_need * sizeof(double));
+        for (int64_t q = q0; q < q1; ++q) {
+          StitchDesc& dsc = descs[q - q0];
+          const Index L = dsc.L;
+          Index rc[kMaxP];
+          for (int m = 0; m < p; ++m) rc[m] = t->clamped(m, L);
+          if (where == TT_MEM_DEVICE) {
+            for (int m = 0; m < p; ++m) dsc.out_f[m] = outs[q].factors[m];
+            dsc.out_core = outs[q].core;
+          } else {
+            double* cur = t->qout.as<double>() + out_off[q - q0];
+            auto take = [&cur](Index nd) {
+              double* r = cur;
+              cur += (nd + 31) & ~Index(31);
+              return r;
+            };
+            dsc.out_f[0] = take(L * rc[0]);
+            for (int m = 1; m < p; ++m) dsc.out_f[m] = take(t->d[m] * rc[m]);
+            dsc.out_core = take(prod_range(rc, 0, p));
           }
         }
       }
-      const auto st = run_stitch_batch(ex, prm, descs, parts, ws);
+      // Waves: with DMA'd outputs the chunk runs as a few launches of growing
+      // size so the PCIe download (the end-to-end bound) starts after a short
+      // first wave and overlaps the rest. Wave 0 holds the cheapest queries
+      // (it finishes fastest); later waves are runs in query order, which keeps
+      // their outputs host-contiguous for large copies.
+      std::vector<int64_t> order(static_cast<size_t>(nc));
+      for (int64_t i = 0; i < nc; ++i) order[i] = i;
+      std::vector<int64_t> wave_end;
+      if (dma && nc >= 64) {
+        auto qcost = [&](int64_t i) { return double(descs[i].L) + 4096.0 * descs[i].nparts; };
+        std::vector<int64_t> by_cost(order);
+        std::stable_sort(by_cost.begin(), by_cost.end(), [&](int64_t x, int64_t y) { return qcost(x) < qcost(y); });
+        const int64_t w0 = (nc + 31) / 32;
+        std::vector<char> first(static_cast<size_t>(nc), 0);
+        for (int64_t j = 0; j < w0; ++j) first[by_cost[j]] = 1;
+        int64_t j = 0;
+        for (int64_t i = 0; i < nc; ++i)
+          if (first[i]) order[j++] = i;
+        for (int64_t i = 0; i < nc; ++i)
+          if (!first[i]) order[j++] = i;
+        int64_t w = w0, e = 0;
+        while (e < nc) {
+          e = std::min(nc, e + w);
+          if (nc - e < w || static_cast<int>(wave_end.size()) == Exec::kWaveEvents - 1) e = nc;
+          wave_end.push_back(e);
+          w *= 2;
+        }
+      } else {
+        wave_end.push_back(nc);
+      }
+      // per chunk-relative query: its output refs (for the wave downloads)
+      std::vector<std::vector<size_t>> q_refs(static_cast<size_t>(nc));
+      for (size_t i = 0; i < orefs.size(); ++i) q_refs[orefs[i].q].push_back(i);
+      std::vector<ProblemStatus> st(static_cast<size_t>(nc));
+      int64_t wb = 0;
+      for (size_t wi = 0; wi < wave_end.size(); ++wi) {
+        const int64_t we = wave_end[wi];
+        if (wave_end.size() == 1) {  // one launch over the whole chunk, no reordering
+          st = run_stitch_batch(ex, prm, descs, parts, ws);
+          if (dma) {
+            cuda_check(cudaEventRecord(ex.wave_ev[0], ex.stream), "event");
+            cuda_check(cudaStreamWaitEvent(ex.copy, ex.wave_ev[0], 0), "cudaStreamWaitEvent");
+          }
+        }
+        std::vector<StitchDesc> wd;
+        std::vector<StitchPart> wp;
+        std::vector<Index> wws;
+        for (int64_t j = wb; j < we && wave_end.size() > 1; ++j) {
+          StitchDesc d = descs[order[j]];
+          const int32_t p0 = d.part0;
+          d.part0 = static_cast<int32_t>(wp.size());
+          wp.insert(wp.end(), parts.begin() + p0, parts.begin() + p0 + d.nparts);
+          wd.push_back(d);
+          wws.push_back(ws[order[j]]);
+        }
+        if (wave_end.size() > 1) {
+          auto wst = run_stitch_batch(ex, prm, wd, wp, wws);
+          for (int64_t j = wb; j < we; ++j) st[order[j]] = std::move(wst[j - wb]);
+        }
+        if (dma && wave_end.size() > 1) {
+          cuda_check(cudaEventRecord(ex.wave_ev[wi], ex.stream), "event");
+          cuda_check(cudaStreamWaitEvent(ex.copy, ex.wave_ev[wi], 0), "cudaStreamWaitEvent");
+        }
+        if (dma) {
+          std::vector<size_t> wr;
+          for (int64_t j = wb; j < we; ++j) wr.insert(wr.end(), q_refs[order[j]].begin(), q_refs[order[j]].end());
+          std::sort(wr.begin(), wr.end(), [&](size_t x, size_t y) { return orefs[x].host < orefs[y].host; });
+          size_t r = 0;
+          while (r < wr.size()) {  // merge runs adjacent in host memory and in staging
+            char* h0 = orefs[wr[r]].host;
+            const size_t s0 = stage_off[wr[r]];
+            size_t len = orefs[wr[r]].bytes;
+            size_t r2 = r + 1;
+            while (r2 < wr.size() && orefs[wr[r2]].host == h0 + len && stage_off[wr[r2]] == s0 + len &&
+                   (len & 7) == 0) {
+              len += orefs[wr[r2]].bytes;
+              ++r2;
+            }
+            cuda_check(cudaMemcpyAsync(h0, t->qout.as<char>() + s0, len, cudaMemcpyDeviceToHost, ex.copy),
+                       "query output download");
+            r = r2;
+          }
+        }
+        wb = we;
+      }
       std::vector<CopySeg> segs;
       bool all_mapped = where == TT_MEM_HOST;
       for (int64_t q = q0; q < q1; ++q) {
@@ -1303,8 +1473,9 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
         if (s.zero) {
           for (int m = 0; m < p; ++m) k[m] = t->clamped(m, L);
           const auto u0 = t->init.stitch_zero_u0(L, k[0]);
-          if (u0_direct[q - q0]) {
-            std::memcpy(o.factors[0], u0.data(), u0.size() * sizeof(double));
+          if (dma) {
+            ex.sync_copy();  // the wave's download of the staging rows must land first
+            if (o.factors[0]) std::memcpy(o.factors[0], u0.data(), u0.size() * sizeof(double));
           } else {
             cuda_check(cudaMemcpyAsync(descs[q - q0].out_f[0], u0.data(), u0.size() * sizeof(double),
                                        cudaMemcpyHostToDevice, ex.stream),
@@ -1317,7 +1488,7 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
         o.converged = s.converged;
         o.objective = s.objective.empty() ? 0.0 : s.objective.back();
         o.nhits = static_cast<int32_t>(hits[q].size());
-        if (where == TT_MEM_HOST) {
+        if (where == TT_MEM_HOST && !dma) {
           const StitchDesc& dsc = descs[q - q0];
           // small outputs: one gather kernel into mapped host memory when every
           // destination is pinned, else individual copies
@@ -1335,7 +1506,7 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
           };
           add(o.core, dsc.out_core, prod_range(k, 0, p));
           for (int m = 1; m < p; ++m) add(o.factors[m], dsc.out_f[m], t->d[m] * k[m]);
-          if (!u0_direct[q - q0]) add(o.factors[0], dsc.out_f[0], L * k[0]);
+          add(o.factors[0], dsc.out_f[0], L * k[0]);
         }
       }
       if (!segs.empty()) {
@@ -1348,6 +1519,7 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
       }
       (void)all_mapped;
       ex.sync();
+      ex.sync_copy();  // qout is reused by the next chunk
       q0 = q1;
     }
     cuda_check(cudaEventRecord(ex.ev[2], ex.stream), "event");

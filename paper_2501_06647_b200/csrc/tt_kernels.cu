@@ -275,7 +275,7 @@ constexpr int kSiMaxIter = 40;
 // start of the subspace-iteration state in dynamic shared memory: after the
 // per-warp partial sums (nwarps x kSiMaxYK) and the Rayleigh-Ritz eigensolver
 // scratch (3 * 16^2)
-__device__ __forceinline__ int si_base() { return imax(int(blockDim.x >> 5) * 512, 768); }
+__device__ __forceinline__ constexpr int si_base() { return kWarps * 512; }
 constexpr int kSiMaxK = 16;     // register-tile bound on k
 constexpr int kSiMaxYK = 512;   // bound on cols * k (16 outputs per lane)
 
@@ -821,7 +821,7 @@ __device__ __noinline__ void materialize_u0_k(const StitchPart* __restrict__ par
         const int c = threadIdx.x;
         double b = sc.red[c];
         int64_t bi = idxbuf[c];
-        for (int ww = 1; ww < int(blockDim.x >> 5); ++ww) {
+        for (int ww = 1; ww < kWarps; ++ww) {
           const double ob = sc.red[ww * kMaxVec + c];
           const int64_t oi = idxbuf[ww * kMaxVec + c];
           const int64_t ai = bi < 0 ? -bi : bi, ao = oi < 0 ? -oi : oi;
@@ -876,264 +876,6 @@ __device__ __forceinline__ PartView load_part(const StitchPart& s) {
   v.len = s.len;
   v.partial = s.partial;
   return v;
-}
-
-// ---------------------------------------------------------------------------
-// Mode-0 subspace iteration of the stitch in compressed coordinates, fused over
-// all parts: the rows of every part's E_i (rho_i x K, per-part slots) form one
-// stacked index g, so each step below is one block-wide pass with one barrier
-// instead of one small GEMM per part. E^T S E = I defines orthonormality
-// (S = blockdiag(S_i), S_i = I for entire parts).
-struct M0Ctx {
-  const StitchPart* parts;
-  int s;
-  int64_t Q;
-  double* Cb;  // C_i = Cb + i*Cs: rho_i x Q row-major
-  int64_t Cs;
-  double* Sb;  // S_i: rho_i x rho_i col-major
-  int64_t Ss;
-  double* Eb;  // E_i, A_i (= S_i E_i), E2_i: rho_i x K col-major, stride Es
-  double* Ab;
-  double* E2b;
-  int64_t Es;
-  double* Rt;  // scratch (sum rho x K)
-  bool init_from_c;
-};
-
-template <int K>
-__device__ __noinline__ int mode0_si_k(const M0Ctx& c, double* dsm, double* misc, BlockScratch& sc) {
-  const int s = c.s;
-  const int64_t Q = c.Q;
-  double* Y = dsm + si_base();               // Q x K
-  double* small = Y + kSiMaxYK;              // G, L, Linv (K x K each)
-  double* B = small + 4 * K * K;             // K x K
-  int* pl = reinterpret_cast<int*>(small + 5 * K * K);  // stacked row -> part | (row in part << 8)
-  __shared__ int rho_s[64], part_partial[64];
-  __shared__ int nrows;
-  if (threadIdx.x == 0) {
-    int g = 0;
-    for (int i = 0; i < s; ++i) {
-      rho_s[i] = int(c.parts[i].rho[0]);
-      part_partial[i] = c.parts[i].partial;
-      for (int a = 0; a < rho_s[i]; ++a, ++g) {
-        pl[g] = i | (a << 8);
-      }
-    }
-    nrows = g;
-  }
-  __syncthreads();
-  const int R = nrows;
-  auto E = [&](int i) { return c.Eb + int64_t(i) * c.Es; };
-  auto A = [&](int i) { return c.Ab + int64_t(i) * c.Es; };
-  auto E2 = [&](int i) { return c.E2b + int64_t(i) * c.Es; };
-  auto C = [&](int i) { return c.Cb + int64_t(i) * c.Cs; };
-  auto S = [&](int i) { return c.Sb + int64_t(i) * c.Ss; };
-  // A = S E (entire parts: A = E)
-  auto pass_AS = [&]() {
-    for (int e = threadIdx.x; e < R * K; e += blockDim.x) {
-      const int g = e % R, j = e / R, i = pl[g] & 255, a = pl[g] >> 8, r = rho_s[i];
-      const double* Ei = E(i) + j * r;
-      double v;
-      if (part_partial[i]) {
-        const double* Si = S(i) + a;
-        v = 0.0;
-        for (int b = 0; b < r; ++b) v = fma(Si[b * r], Ei[b], v);
-      } else {
-        v = Ei[a];
-      }
-      A(i)[a + j * r] = v;
-    }
-    __syncthreads();
-  };
-  // E <- E L^{-T} with E^T S E = L L^T (two passes = CholeskyQR2 in the S metric)
-  auto s_orth = [&]() -> bool {
-    for (int pass = 0; pass < 2; ++pass) {
-      pass_AS();
-      double* G = small;
-      for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
-        const int j = e % K, l = e / K;
-        double v = 0.0;
-        for (int g = 0; g < R; ++g) {
-          const int i = pl[g] & 255, a = pl[g] >> 8, r = rho_s[i];
-          v = fma(E(i)[a + j * r], A(i)[a + l * r], v);
-        }
-        G[e] = v;
-      }
-      if (threadIdx.x == 0) sc.ibcast[2] = 0;
-      __syncthreads();
-      chol_inv_warp(G, K, small + K * K, small + 2 * K * K, sc);
-      __syncthreads();
-      if (sc.ibcast[2]) return false;
-      const double* Li = small + 2 * K * K;
-      for (int g = threadIdx.x; g < R; g += blockDim.x) {
-        const int i = pl[g] & 255, a = pl[g] >> 8, r = rho_s[i];
-        double* Ei = E(i) + a;
-        double w[K];
-#pragma unroll
-        for (int l = 0; l < K; ++l) w[l] = Ei[l * r];
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-          double v = 0.0;
-#pragma unroll
-          for (int l = 0; l <= j; ++l) v = fma(w[l], Li[j + l * K], v);
-          Ei[j * r] = v;
-        }
-      }
-      __syncthreads();
-    }
-    return true;
-  };
-  if (c.init_from_c) {
-    // start: the K columns of C with the largest S-norm
-    double* cn = misc + kMisc / 2;
-    for (int64_t q = threadIdx.x; q < Q; q += blockDim.x) {
-      double v = 0.0;
-      for (int i = 0; i < s; ++i) {
-        const int r = rho_s[i];
-        const double* Ci = C(i);
-        if (part_partial[i]) {
-          const double* Si = S(i);
-          for (int a = 0; a < r; ++a)
-            for (int b = 0; b < r; ++b) v = fma(Ci[a * Q + q] * Si[a + b * r], Ci[b * Q + q], v);
-        } else {
-          for (int a = 0; a < r; ++a) v = fma(Ci[a * Q + q], Ci[a * Q + q], v);
-        }
-      }
-      cn[q] = v;
-    }
-    __syncthreads();
-    int* pick = reinterpret_cast<int*>(misc);
-    for (int64_t q = threadIdx.x; q < Q; q += blockDim.x) {
-      int rank = 0;
-      for (int64_t l = 0; l < Q; ++l) rank += (cn[l] > cn[q] || (cn[l] == cn[q] && l < q));
-      if (rank < K) pick[rank] = int(q);
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < R * K; e += blockDim.x) {
-      const int g = e % R, j = e / R, i = pl[g] & 255, a = pl[g] >> 8, r = rho_s[i];
-      E(i)[a + j * r] = C(i)[a * Q + pick[j]];
-    }
-    __syncthreads();
-    if (!s_orth()) return -1;
-  }
-  int iters = -1;
-  for (int it = 0; it < kSiMaxIter; ++it) {
-    pass_AS();
-    // Y = C^T A  (Q x K)
-    for (int64_t e = threadIdx.x; e < Q * K; e += blockDim.x) {
-      const int64_t q = e % Q, j = e / Q;
-      double v = 0.0;
-      for (int g = 0; g < R; ++g) {
-        const int i = pl[g] & 255, a = pl[g] >> 8, r = rho_s[i];
-        v = fma(C(i)[a * Q + q], A(i)[a + j * r], v);
-      }
-      Y[e] = v;
-    }
-    __syncthreads();
-    // B = Y^T Y
-    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
-      const int j = e % K, l = e / K;
-      double v = 0.0;
-      for (int64_t q = 0; q < Q; ++q) v = fma(Y[q + j * Q], Y[q + l * Q], v);
-      B[e] = v;
-    }
-    __syncthreads();
-    // W = C Y (into E2) and R = W - E B (into Rt)
-    for (int g = threadIdx.x; g < R; g += blockDim.x) {
-      const int i = pl[g] & 255, a = pl[g] >> 8, r = rho_s[i];
-      const double* Ci = C(i) + a * Q;
-      double w[K];
-#pragma unroll
-      for (int j = 0; j < K; ++j) w[j] = 0.0;
-      for (int64_t q = 0; q < Q; ++q) {
-        const double cv = Ci[q];
-#pragma unroll
-        for (int j = 0; j < K; ++j) w[j] = fma(cv, Y[q + j * Q], w[j]);
-      }
-      double ev[K];
-#pragma unroll
-      for (int l = 0; l < K; ++l) ev[l] = E(i)[a + l * r];
-#pragma unroll
-      for (int j = 0; j < K; ++j) {
-        E2(i)[a + j * r] = w[j];
-        double v = w[j];
-#pragma unroll
-        for (int l = 0; l < K; ++l) v = fma(-ev[l], B[l + j * K], v);
-        c.Rt[g + j * R] = v;
-      }
-    }
-    __syncthreads();
-    // rsq = <R, S R>
-    double rsq = 0.0;
-    for (int e = threadIdx.x; e < R * K; e += blockDim.x) {
-      const int g = e % R, j = e / R, i = pl[g] & 255, a = pl[g] >> 8, r = rho_s[i];
-      const double rv = c.Rt[e];
-      if (part_partial[i]) {
-        const double* Si = S(i) + a;
-        const int g0 = g - a;
-        double sr = 0.0;
-        for (int b = 0; b < r; ++b) sr = fma(Si[b * r], c.Rt[g0 + b + j * R], sr);
-        rsq = fma(rv, sr, rsq);
-      } else {
-        rsq = fma(rv, rv, rsq);
-      }
-    }
-    double bsq = 0.0;
-    for (int e = threadIdx.x; e < K * K; e += blockDim.x) bsq = fma(B[e], B[e], bsq);
-    rsq = block_sum(rsq, sc);
-    bsq = block_sum(bsq, sc);
-    if (!(bsq > 0.0)) return -1;
-    if (rsq <= 1e-26 * bsq) {
-      iters = it + 1;
-      break;
-    }
-    for (int e = threadIdx.x; e < R * K; e += blockDim.x) {
-      const int g = e % R, j = e / R, i = pl[g] & 255, a = pl[g] >> 8, r = rho_s[i];
-      E(i)[a + j * r] = E2(i)[a + j * r];
-    }
-    __syncthreads();
-    if (!s_orth()) return -1;
-  }
-  if (iters < 0) return -1;
-  // Rayleigh-Ritz: E <- E R (descending), A = S E
-  int* order = reinterpret_cast<int*>(misc);
-  double* diag = nullptr;
-  const double* Rr = eig_run(B, K, small, order, dsm, &diag, sc);
-  for (int g = threadIdx.x; g < R; g += blockDim.x) {
-    const int i = pl[g] & 255, a = pl[g] >> 8, r = rho_s[i];
-    double ev[K];
-#pragma unroll
-    for (int l = 0; l < K; ++l) ev[l] = E(i)[a + l * r];
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-      const double* rj = Rr + int64_t(order[j]) * K;
-      double v = 0.0;
-#pragma unroll
-      for (int l = 0; l < K; ++l) v = fma(ev[l], rj[l], v);
-      E2(i)[a + j * r] = v;
-    }
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < R * K; e += blockDim.x) {
-    const int g = e % R, j = e / R, i = pl[g] & 255, a = pl[g] >> 8, r = rho_s[i];
-    E(i)[a + j * r] = E2(i)[a + j * r];
-  }
-  __syncthreads();
-  pass_AS();
-  return iters;
-}
-
-__device__ int mode0_si(int k, const M0Ctx& c, double* dsm, double* misc, BlockScratch& sc) {
-  switch (k) {
-#define TT_CASE(N) \
-  case N:          \
-    return mode0_si_k<N>(c, dsm, misc, sc);
-    TT_CASE(1) TT_CASE(2) TT_CASE(3) TT_CASE(4) TT_CASE(5) TT_CASE(6) TT_CASE(7) TT_CASE(8)
-    TT_CASE(9) TT_CASE(10) TT_CASE(11) TT_CASE(12) TT_CASE(13) TT_CASE(14) TT_CASE(15) TT_CASE(16)
-#undef TT_CASE
-    default:
-      return -1;
-  }
 }
 
 __global__ void __launch_bounds__(kStitchThreads, 2)
@@ -1246,31 +988,169 @@ __global__ void __launch_bounds__(kStitchThreads, 2)
       bool mode0_done = false;
       int64_t rho0_sum = 0;
       for (int i = 0; i < s; ++i) rho0_sum += parts[i].rho[0];
-      if (k0n <= kSiMaxK && Q >= 2 * k0n && Q * k0n <= kSiMaxYK && rho0_sum >= k0n && rho0_sum <= 1024 && s <= 64 &&
-          si_base() + kSiMaxYK + 5 * k0n * k0n + (rho0_sum + 1) / 2 <= sc.dsm_cap) {
+      if (k0n <= kSiMaxK && Q >= 2 * k0n && Q * k0n <= kSiMaxYK && rho0_sum >= k0n) {
         const long long t_si = tstart();
-        M0Ctx mc;
-        mc.parts = parts;
-        mc.s = s;
-        mc.Q = Q;
-        mc.Cb = ws + lay.C;
-        mc.Cs = lay.per_part_C;
-        mc.Sb = ws + lay.S;
-        mc.Ss = lay.per_part_S;
-        mc.Eb = ws + lay.E;
-        mc.Ab = ws + lay.A;
-        mc.E2b = ws + lay.E2;
-        mc.Es = lay.per_part_E;
-        mc.Rt = Z;
-        mc.init_from_c = (sweep == 0 || k[0] < k0n);
-        const int it = mode0_si(int(k0n), mc, dsm, misc, sc);
-        if (it > 0) {
+        double* Y = wk;                          // Q x k0
+        double* small = dsm + si_base() + kSiMaxYK;  // 4 k x k (shared memory)
+        double* B = small + 4 * k0n * k0n;       // k x k
+        const int kk = int(k0n);
+        auto apply_S = [&](int i, const double* X, double* out) {  // out = S_i X (rho0 x k)
+          const int64_t r0 = parts[i].rho[0];
+          if (parts[i].partial) {
+            gemm(r0, kk, r0, Sp(i), 1, r0, X, 1, r0, out, 1, r0, false, sc);
+          } else if (out != X) {
+            bcopy(out, X, r0 * kk);
+          }
+        };
+        // S-orthonormalise E (two CholeskyQR passes with the metric S)
+        auto s_orth = [&]() -> bool {
+          for (int pass = 0; pass < 2; ++pass) {
+            double* G = small;
+            double* L = small + kk * kk;
+            double* Li = small + 2 * kk * kk;
+            for (int i = 0; i < s; ++i) {
+              const int64_t r0 = parts[i].rho[0];
+              apply_S(i, Ep(i), Ap(i));
+              gemm(kk, kk, r0, Ep(i), r0, 1, Ap(i), 1, r0, G, 1, kk, i > 0, sc);
+            }
+            if (threadIdx.x == 0) sc.ibcast[2] = 0;
+            __syncthreads();
+            chol_inv_warp(G, kk, L, Li, sc);
+            __syncthreads();
+            if (sc.ibcast[2]) return false;
+            for (int i = 0; i < s; ++i) {
+              const int64_t r0 = parts[i].rho[0];
+              double* E = Ep(i);
+              for (int64_t r = threadIdx.x; r < r0; r += blockDim.x) {
+                double w[kSiMaxK];
+#pragma unroll
+                for (int l = 0; l < kSiMaxK; ++l) w[l] = l < kk ? E[r + l * r0] : 0.0;
+                for (int j = 0; j < kk; ++j) {
+                  double v = 0.0;
+#pragma unroll
+                  for (int l = 0; l < kSiMaxK; ++l)
+                    if (l <= j) v = fma(w[l], Li[j + l * kk], v);
+                  E[r + j * r0] = v;
+                }
+              }
+            }
+            __syncthreads();
+          }
+          return true;
+        };
+        bool ok = true;
+        if (sweep == 0 || k[0] < k0n) {
+          // start: the k0 columns of C with the largest S-norm
+          double* cn = misc + kMisc / 2;  // Q norms
+          for (int64_t j = threadIdx.x; j < Q; j += blockDim.x) cn[j] = 0.0;
+          __syncthreads();
+          for (int i = 0; i < s; ++i) {
+            const int64_t r0 = parts[i].rho[0];
+            const double* Ci = Cp(i);
+            for (int64_t j = threadIdx.x; j < Q; j += blockDim.x) {
+              double v = 0.0;
+              if (parts[i].partial) {
+                const double* S = Sp(i);
+                for (int64_t a = 0; a < r0; ++a)
+                  for (int64_t b = 0; b < r0; ++b) v = fma(Ci[a * Q + j] * S[a + b * r0], Ci[b * Q + j], v);
+              } else {
+                for (int64_t a = 0; a < r0; ++a) v = fma(Ci[a * Q + j], Ci[a * Q + j], v);
+              }
+              cn[j] += v;
+            }
+            __syncthreads();
+          }
+          int* pick = reinterpret_cast<int*>(misc);
+          for (int64_t j = threadIdx.x; j < Q; j += blockDim.x) {
+            int rank = 0;
+            for (int64_t l = 0; l < Q; ++l) rank += (cn[l] > cn[j] || (cn[l] == cn[j] && l < j));
+            if (rank < kk) pick[rank] = int(j);
+          }
+          __syncthreads();
+          for (int i = 0; i < s; ++i) {
+            const int64_t r0 = parts[i].rho[0];
+            const double* Ci = Cp(i);
+            double* E = Ep(i);
+            for (int64_t idx = threadIdx.x; idx < r0 * kk; idx += blockDim.x) {
+              const int64_t a = idx % r0, c = idx / r0;
+              E[idx] = Ci[a * Q + pick[c]];
+            }
+          }
+          __syncthreads();
+          ok = s_orth();
+        } else if (k[0] > k0n) {
+          // previous E has more columns (ld rho0): keep the first k0n (same ld)
+          ok = true;
+        }
+        bool conv = false;
+        for (int it = 0; ok && it < kSiMaxIter; ++it) {
+          // A_i = S_i E_i ; Y = sum_i C_i^T A_i (Q x k) ; B = Y^T Y ; W_i = C_i Y
+          for (int i = 0; i < s; ++i) {
+            const int64_t r0 = parts[i].rho[0];
+            apply_S(i, Ep(i), Ap(i));
+            gemm(Q, kk, r0, Cp(i), 1, Q, Ap(i), 1, r0, Y, 1, Q, i > 0, sc);
+          }
+          gram_tall(Y, Q, Q, kk, B);
+          double rsq = 0.0;
+          for (int i = 0; i < s; ++i) {
+            const int64_t r0 = parts[i].rho[0];
+            gemm(r0, kk, Q, Cp(i), Q, 1, Y, 1, Q, E2p(i), 1, r0, false, sc);
+            // R = W - E B (into T[0]); rsq += <R, S R>
+            double* R = T[0];
+            for (int64_t idx = threadIdx.x; idx < r0 * kk; idx += blockDim.x) {
+              const int64_t a = idx % r0, j = idx / r0;
+              double v = E2p(i)[idx];
+              for (int l = 0; l < kk; ++l) v = fma(-Ep(i)[a + l * r0], B[l + j * kk], v);
+              R[idx] = v;
+            }
+            __syncthreads();
+            double part = 0.0;
+            if (parts[i].partial) {
+              gemm(r0, kk, r0, Sp(i), 1, r0, R, 1, r0, HH, 1, r0, false, sc);
+              for (int64_t idx = threadIdx.x; idx < r0 * kk; idx += blockDim.x) part = fma(R[idx], HH[idx], part);
+            } else {
+              for (int64_t idx = threadIdx.x; idx < r0 * kk; idx += blockDim.x) part = fma(R[idx], R[idx], part);
+            }
+            rsq += block_sum(part, sc);
+          }
+          double bsq = 0.0;
+          for (int e = threadIdx.x; e < kk * kk; e += blockDim.x) bsq = fma(B[e], B[e], bsq);
+          bsq = block_sum(bsq, sc);
+          if (!(bsq > 0.0)) {
+            ok = false;
+            break;
+          }
+          if (rsq <= 1e-26 * bsq) {
+            conv = true;
+            if (threadIdx.x == 0) sc.si_iters += it + 1;
+            break;
+          }
+          for (int i = 0; i < s; ++i) bcopy(Ep(i), E2p(i), parts[i].rho[0] * kk);
+          ok = s_orth();
+        }
+        if (ok && conv) {
+          // Rayleigh-Ritz: E <- E R (descending), then A_i = S_i E_i
+          int* order = reinterpret_cast<int*>(misc);
+          double* diag = nullptr;
+          const double* R = eig_run(B, kk, small, order, dsm, &diag, sc);
+          for (int i = 0; i < s; ++i) {
+            const int64_t r0 = parts[i].rho[0];
+            double* E = Ep(i);
+            double* E2 = E2p(i);
+            for (int64_t idx = threadIdx.x; idx < r0 * kk; idx += blockDim.x) {
+              const int64_t a = idx % r0, j = idx / r0;
+              const double* rj = R + int64_t(order[j]) * kk;
+              double v = 0.0;
+              for (int l = 0; l < kk; ++l) v = fma(E[a + l * r0], rj[l], v);
+              E2[idx] = v;
+            }
+            __syncthreads();
+            bcopy(E, E2, r0 * kk);
+            if (parts[i].partial) apply_S(i, E, Ap(i));
+          }
           any_zero_sigma = 0;
           mode0_done = true;
-          if (threadIdx.x == 0) {
-            sc.si_ok += 1;
-            sc.si_iters += it;
-          }
+          if (threadIdx.x == 0) sc.si_ok += 1;
         } else if (threadIdx.x == 0) {
           sc.si_fail += 1;
         }
@@ -1369,7 +1249,8 @@ __global__ void __launch_bounds__(kStitchThreads, 2)
         const int64_t Qn = zo * zi;
         int64_t rho_n_sum = 0;
         for (int i = 0; i < s; ++i) rho_n_sum += parts[i].rho[n];
-        const bool one_pass = rho_n_sum * Qn <= int64_t(sc.dsm_cap) && s <= 64;
+        // (two-part append stitches are faster part by part)
+        const bool one_pass = rho_n_sum * Qn <= int64_t(sc.dsm_cap) && s >= 3 && s <= 64;
         for (int i = 0; i < s; ++i) {
           const PartView pv = load_part(parts[i]);
           int64_t cur[kMaxP];
@@ -1553,7 +1434,7 @@ __global__ void __launch_bounds__(kStitchThreads, 2)
           const int c = threadIdx.x;
           double b = sc.red[c];
           int64_t bi = idxbuf[c];
-          for (int ww = 1; ww < int(blockDim.x >> 5); ++ww) {
+          for (int ww = 1; ww < kWarps; ++ww) {
             const double ob = sc.red[ww * kMaxVec + c];
             const int64_t oi = idxbuf[ww * kMaxVec + c];
             if (ob > b || (ob == b && oi < bi)) {

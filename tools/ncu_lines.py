@@ -14,8 +14,12 @@ import sys
 def main():
     rep = sys.argv[1]
     top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                         capture_output=True, text=True).stdout
+    if rep.endswith(".csv.gz"):  # page exported on the GPU box
+        import gzip
+        out = gzip.open(rep, "rt").read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                             capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     agg, text = {}, {}
     fname = None
