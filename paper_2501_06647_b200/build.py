@@ -14,8 +14,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libtucktree_b200.so")
-SOURCES = ["tt_kernels.cu", "tt_host.cpp"]
-HEADERS = ["tt_common.h", "tt_block.cuh"]
+SOURCES = ["tt_leaf.cu", "tt_stitch.cu", "tt_host.cpp"]
+HEADERS = ["tt_common.h", "tt_block.cuh", "tt_dev.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -35,15 +35,29 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
     extra = ["-DTT_INSTRUMENT"] if os.environ.get("TT_INSTRUMENT") == "1" else []
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O3", *extra,
-           "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(ROOT, "include"),
-           *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp"]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", *extra,
+              "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(ROOT, "include")]
+    # one translation unit per kernel family, compiled in parallel, then linked
+    objs, procs = [], []
+    for src in SOURCES:
+        obj = os.path.join(OUT_DIR, os.path.splitext(src)[0] + ".o")
+        objs.append(obj)
+        procs.append(subprocess.Popen(common + ["-c", os.path.join(CSRC, src), "-o", obj],
+                                      stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
+    errs = []
+    for pr in procs:
+        out, err = pr.communicate()
+        if pr.returncode != 0:
+            errs.append(out + err)
+        elif verbose:
+            sys.stderr.write(err)
+    if errs:
+        sys.stderr.write("\n".join(errs))
+        raise RuntimeError("nvcc failed building libtucktree_b200.so")
+    r = subprocess.run([NVCC, *ARCH, "-shared", *objs, "-o", LIB + ".tmp"], capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libtucktree_b200.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("nvcc failed linking libtucktree_b200.so")
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

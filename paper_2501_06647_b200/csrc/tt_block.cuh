@@ -264,6 +264,7 @@ __device__ __forceinline__ void gram_tall(const double* __restrict__ V, int64_t 
     double acc[PB];
 #pragma unroll
     for (int u = 0; u < PB; ++u) acc[u] = 0.0;
+#pragma unroll 4
     for (int64_t r = lane; r < rows; r += 32) {
 #pragma unroll
       for (int u = 0; u < PB; ++u) acc[u] = fma(V[r + pi[u] * ld], V[r + pj[u] * ld], acc[u]);
@@ -326,7 +327,7 @@ __device__ __forceinline__ void gram_cols(const double* __restrict__ P, int64_t 
 // (ties by lower index). One round rotates n/2 disjoint planes at once; each
 // 2x2 block of A and each row pair of V is owned by one thread, so a round is
 // two barriers.
-__device__ int sym_eig(double* A, int n, double* V, int* order, BlockScratch& sc) {
+static __device__ int sym_eig(double* A, int n, double* V, int* order, BlockScratch& sc) {
   const int n2 = n + (n & 1);
   const int np = n2 / 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -483,7 +484,7 @@ __device__ __forceinline__ void rr_pair(int r, int k, int n2, int& p, int& q) {
   }
 }
 
-__device__ int sym_eig_smem(double* S, int n, int* order, BlockScratch& sc) {
+static __device__ int sym_eig_smem(double* S, int n, int* order, BlockScratch& sc) {
   const int n2 = n + (n & 1);
   const int np = n2 / 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -616,7 +617,7 @@ __device__ int sym_eig_smem(double* S, int n, int* order, BlockScratch& sc) {
 
 // Sign convention of linalg.cpp:15-31: each column's first max-|.| entry is
 // made nonnegative. flips[j] = 1 when column j was negated.
-__device__ void sign_fix(double* U, int64_t rows, int k, int64_t ld, int* flips, BlockScratch& sc) {
+static __device__ void sign_fix(double* U, int64_t rows, int k, int64_t ld, int* flips, BlockScratch& sc) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   for (int j = 0; j < k; ++j) {
     double best = -1.0;
@@ -671,7 +672,7 @@ __device__ void sign_fix(double* U, int64_t rows, int k, int64_t ld, int* flips,
 // Classical Gram-Schmidt applied twice (CGS2) to columns [j0, k) of U against
 // all earlier columns; a column whose norm collapses (rank-deficient input) is
 // replaced by the first unit vector e_r that survives orthogonalisation.
-__device__ void orthonormalize(double* U, int64_t rows, int j0, int k, int64_t ld, BlockScratch& sc) {
+static __device__ void orthonormalize(double* U, int64_t rows, int j0, int k, int64_t ld, BlockScratch& sc) {
   for (int j = j0; j < k; ++j) {
     double* uj = U + int64_t(j) * ld;
     int64_t next_e = 0;

@@ -159,7 +159,8 @@ TT_HD LeafWs leaf_ws_layout(int p, int64_t len, const int64_t* d, const int64_t*
 }
 
 struct StitchWs {
-  int64_t P, C, S, E, A, E2, G, V, T1, T2, Z, WK, HH, SI, misc, total, gram_n;
+  int64_t P, C, S, E, A, E2, G, V, T1, T2, TB1, TB2, Z, WK, HH, SI, misc, total, gram_n;
+  int64_t chain;  // per-part stride of the part-batched mode-product chains (TB1/TB2)
   int64_t per_part_P, per_part_C, per_part_S, per_part_E;
 };
 
@@ -196,7 +197,10 @@ TT_HD StitchWs stitch_ws_layout(int p, int64_t L, const int64_t* d, const int64_
   w.V = w.G + g * g;
   w.T1 = w.V + g * g;
   w.T2 = w.T1 + chain;
-  w.Z = w.T2 + chain;
+  w.chain = chain;
+  w.TB1 = w.T2 + chain;
+  w.TB2 = w.TB1 + int64_t(nparts) * chain;
+  w.Z = w.TB2 + int64_t(nparts) * chain;
   w.WK = w.Z + z;
   w.HH = w.WK + g * rc[0];
   int64_t maxrows = 1, kmax = 1;

@@ -1,0 +1,582 @@
+// Shared device helpers of the sm_100a ALS kernels (tt_leaf.cu, tt_stitch.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include <atomic>
+
+#include "tt_block.cuh"
+
+namespace ttb {
+
+constexpr int kEigSmemN = 64;  // Jacobi runs in shared memory up to this size
+constexpr int kStitchThreads = 256;  // 2 stitch CTAs per SM (128 threads x 4 CTAs measured slower)
+#ifndef TT_STITCH_CTAS
+#define TT_STITCH_CTAS 2
+#endif
+constexpr int kStitchCtas = TT_STITCH_CTAS;  // resident stitch CTAs per SM (register budget)
+// stitch kernel dynamic shared memory: 64 KB at 2 CTAs/SM, 55 KB at 3
+constexpr size_t kDynSmem = kStitchCtas >= 3 ? size_t(55) * 1024 : size_t(2) * kEigSmemN * kEigSmemN * sizeof(double);
+
+__device__ __forceinline__ unsigned dyn_smem_doubles() {
+  unsigned b;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(b));
+  return b / 8u;
+}
+
+// Leaf streaming ring: kStages tiles of kTileD doubles, plus U^T staging.
+constexpr int kStages = 3;
+constexpr int kTileD = int(kStreamTileDoubles);   // 20 KB per stage
+constexpr int kUStage = 4096;  // U^T staged in shared memory when d*r <= this (32 KB)
+constexpr size_t kLeafDynSmem = size_t(kStages * kTileD + kUStage) * sizeof(double);  // 96 KB
+
+struct Pipe {
+  uint64_t full[kStages];
+  uint32_t uses[kStages];  // completed fills per stage (phase parity)
+};
+
+// out[o][a][t] = sum_j U[j][a] in[o][j][t]  (in: row-major (outer, d, inner);
+// U: d x r col-major, ld d; r <= 16), streaming `in` from global memory through
+// a kStages-deep cp.async.bulk ring. A tile is (G slabs) x (cj rows of j) x
+// (tw columns of t); each thread owns one output column (g, t) and keeps its r
+// accumulators across the j-tiles. Optionally accumulates sum(in^2) (every
+// element is consumed by exactly one thread). Requires 16-byte aligned rows
+// (inner*8 and tw*8 multiples of 16, 16-aligned base).
+template <int R>
+__device__ __noinline__ void ttm_stream_r(const double* __restrict__ in, int64_t outer, int64_t d, int64_t inner,
+                                          const double* __restrict__ U, double* __restrict__ out, double* dyn,
+                                          Pipe& pp, double* norm_acc, const void* tmap, int tmap_rank) {
+  constexpr int r = R;
+  const StreamTile tile = stream_tile(outer, d, inner);
+  const int64_t tw = tile.tw, G = tile.G, cj = tile.cj;
+  const int64_t ngrp = (outer + G - 1) / G, ntt = (inner + tw - 1) / tw, njt = (d + cj - 1) / cj;
+  const int64_t ntiles = ngrp * ntt * njt;
+  double* ring = dyn;
+  double* Ut = dyn + kStages * kTileD;
+  const bool u_smem = d * r <= kUStage;
+  if (u_smem) {  // U^T, j-major: Ut[j*r + a]
+    for (int64_t idx = threadIdx.x; idx < d * r; idx += blockDim.x) {
+      const int64_t j = idx / r, a = idx - j * r;
+      Ut[idx] = U[j + a * d];
+    }
+  }
+  fence_proxy_async();  // prior generic smem accesses vs. the bulk-copy writes below
+  __syncthreads();
+  auto issue = [&](int64_t t) {  // warp 0: fill the stage of tile t
+    const int st = int(t % kStages);
+    const int64_t jt = t % njt, rest = t / njt, tt = rest % ntt, grp = rest / ntt;
+    const int64_t o0 = grp * G, g_n = imin(G, outer - o0);
+    const int64_t j0 = jt * cj, jn = imin(cj, d - j0);
+    const int64_t t0 = tt * tw, tn = imin(tw, inner - t0);
+    double* dst = ring + int64_t(st) * kTileD;
+    const int lane = threadIdx.x & 31;
+    if (tmap != nullptr) {
+      // one TMA box per tile: (tw, cj, G) over (t, j, o); out-of-bounds parts are
+      // zero-filled and still count toward the transaction bytes
+      if (lane == 0) {
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&pp.full[st], uint32_t(G * cj * tw * sizeof(double)));
+        if (tmap_rank == 3)
+          tma_load_3d(dst, tmap, int(t0), int(j0), int(o0), &pp.full[st]);
+        else
+          tma_load_2d(dst, tmap, int(t0), int(j0), &pp.full[st]);
+      }
+      (void)g_n;
+      (void)jn;
+      (void)tn;
+      return;
+    }
+    const bool whole_rows = (tn == inner);  // one contiguous segment per slab
+    const int64_t nseg = whole_rows ? g_n : g_n * jn;
+    const uint32_t seg_bytes = uint32_t((whole_rows ? jn * inner : tn) * sizeof(double));
+    if (lane == 0) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&pp.full[st], uint32_t(nseg) * seg_bytes);
+    }
+    __syncwarp();
+    for (int64_t sg = lane; sg < nseg; sg += 32) {
+      int64_t g, jj;
+      if (whole_rows) {
+        g = sg;
+        jj = 0;
+      } else {
+        g = sg / jn;
+        jj = sg - g * jn;
+      }
+      const double* src = in + ((o0 + g) * d + j0 + jj) * inner + t0;
+      bulk_g2s(dst + (g * cj + jj) * tw, src, seg_bytes, &pp.full[st]);
+    }
+  };
+  if (threadIdx.x < 32)
+    for (int64_t t = 0; t < imin(int64_t(kStages), ntiles); ++t) issue(t);
+  double acc[R];
+  double nrm = 0.0;
+  for (int64_t t = 0; t < ntiles; ++t) {
+    const int st = int(t % kStages);
+    const int64_t jt = t % njt, rest = t / njt, tt = rest % ntt, grp = rest / ntt;
+    const int64_t o0 = grp * G, g_n = imin(G, outer - o0);
+    const int64_t j0 = jt * cj, jn = imin(cj, d - j0);
+    const int64_t t0 = tt * tw, tn = imin(tw, inner - t0);
+    const int64_t g = threadIdx.x / tw, tl = threadIdx.x - g * tw;
+    const bool active = threadIdx.x < G * tw && g < g_n && tl < tn;
+    if (jt == 0) {
+#pragma unroll
+      for (int a = 0; a < R; ++a) acc[a] = 0.0;
+    }
+    mbar_wait(&pp.full[st], pp.uses[st] & 1u);
+    if (active) {
+      // whole-row tiles are packed with row length inner == tn
+      const double* x = ring + int64_t(st) * kTileD + g * cj * tw + tl;
+      if (u_smem) {
+        for (int64_t jj = 0; jj < jn; ++jj) {
+          const double xv = x[jj * tw];
+          if (norm_acc) nrm = fma(xv, xv, nrm);
+          const double* ur = Ut + (j0 + jj) * R;
+#pragma unroll
+          for (int a = 0; a < R; ++a) acc[a] = fma(ur[a], xv, acc[a]);
+        }
+      } else {
+        for (int64_t jj = 0; jj < jn; ++jj) {
+          const double xv = x[jj * tw];
+          if (norm_acc) nrm = fma(xv, xv, nrm);
+#pragma unroll
+          for (int a = 0; a < R; ++a) acc[a] = fma(__ldg(U + (j0 + jj) + a * d), xv, acc[a]);
+        }
+      }
+      if (jt == njt - 1) {
+        double* dst = out + (o0 + g) * r * inner + t0 + tl;
+#pragma unroll
+        for (int a = 0; a < R; ++a) dst[a * inner] = acc[a];
+      }
+    }
+    fence_proxy_async();
+    __syncthreads();  // every thread is done with stage st
+    if (threadIdx.x == 0) pp.uses[st] += 1;
+    if (threadIdx.x < 32 && t + kStages < ntiles) issue(t + kStages);
+  }
+  if (norm_acc) *norm_acc += nrm;
+  __syncthreads();
+}
+
+__device__ __forceinline__ void ttm_stream(const double* in, int64_t outer, int64_t d, int64_t inner, const double* U,
+                                           int r, double* out, double* dyn, Pipe& pp, double* norm_acc,
+                                           const void* tmap, int tmap_rank) {
+  switch (r) {
+#define TT_CASE(N) \
+  case N:          \
+    ttm_stream_r<N>(in, outer, d, inner, U, out, dyn, pp, norm_acc, tmap, tmap_rank); \
+    break;
+    TT_CASE(1) TT_CASE(2) TT_CASE(3) TT_CASE(4) TT_CASE(5) TT_CASE(6) TT_CASE(7) TT_CASE(8)
+    TT_CASE(9) TT_CASE(10) TT_CASE(11) TT_CASE(12) TT_CASE(13) TT_CASE(14) TT_CASE(15) TT_CASE(16)
+#undef TT_CASE
+    default:
+      break;
+  }
+}
+
+__device__ __forceinline__ bool stream_ok(const double* in, int64_t inner, int r) {
+  const int64_t tw = imin(inner, 256);
+  return r <= 16 && ((reinterpret_cast<uintptr_t>(in) & 15u) == 0) && ((inner * 8) % 16 == 0) && ((tw * 8) % 16 == 0);
+}
+
+// Thread-per-output-element mode product, for shapes with few output columns.
+__device__ __forceinline__ void ttm_elems(const double* __restrict__ in, int64_t outer, int64_t d, int64_t inner,
+                                          const double* __restrict__ M, int64_t ms_a, int64_t ms_j, int64_t r,
+                                          double* __restrict__ out, bool acc) {
+  const int64_t tot = outer * r * inner;
+  for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
+    const int64_t t = e % inner;
+    const int64_t q = e / inner;
+    const int64_t a = q % r, o = q / r;
+    const double* src = in + o * d * inner + t;
+    const double* ma = M + a * ms_a;
+    double s = 0.0;
+    for (int64_t j = 0; j < d; ++j) s = fma(ma[j * ms_j], src[j * inner], s);
+    out[e] = acc ? out[e] + s : s;
+  }
+  __syncthreads();
+}
+
+// Dispatch: column-parallel when there are enough output columns.
+__device__ __forceinline__ void mode_product(const double* in, int64_t outer, int64_t d, int64_t inner,
+                                             const double* M, int64_t ms_a, int64_t ms_j, int64_t r, double* out,
+                                             bool acc, BlockScratch& sc, int slot = kPhTtm) {
+  const long long t0 = tstart();
+  if (outer * inner >= 2 * int64_t(blockDim.x))
+    ttm(in, outer, d, inner, M, ms_a, ms_j, r, out, acc);
+  else
+    ttm_elems(in, outer, d, inner, M, ms_a, ms_j, r, out, acc);
+  tstop(sc, slot, t0);
+}
+
+// A Gram eigenvalue carries an absolute rounding error ~eps * lambda_max, so
+// singular values below ~sqrt(1e-13) * sigma_max are numerically zero: their
+// columns are completed orthonormally instead of amplified noise.
+__device__ __forceinline__ bool gram_sigma_ok(double lam, double lam_max) {
+  return lam > 1e-13 * lam_max && lam > 0.0;
+}
+
+__device__ __forceinline__ void tgemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t ars, int64_t acs,
+                                      const double* B, int64_t brs, int64_t bcs, double* C, int64_t crs, int64_t ccs,
+                                      bool acc, BlockScratch& sc) {
+  const long long t0 = tstart();
+  gemm(M, N, K, A, ars, acs, B, brs, bcs, C, crs, ccs, acc, sc);
+  tstop(sc, kPhGemm, t0);
+}
+
+// Runs the Jacobi solver on G (n x n), staging through shared memory when it
+// fits. Returns the pointer holding the eigenvectors; *diag receives the
+// pointer to the diagonalised matrix.
+static __device__ double* eig_run(double* G, int n, double* V, int* order, double* dsm, double** diag, BlockScratch& sc) {
+  int sw;
+  double* res;
+  const long long t0 = tstart();
+  if (n <= kFastEigN && 3 * n * n <= sc.dsm_cap) {
+    bcopy(dsm, G, int64_t(n) * n);
+    sw = sym_eig_smem(dsm, n, order, sc);
+    *diag = dsm;
+    res = dsm + 2 * n * n;
+  } else if (2 * n * n <= sc.dsm_cap) {
+    double* As = dsm;
+    double* Vs = dsm + n * n;
+    bcopy(As, G, int64_t(n) * n);
+    sw = sym_eig(As, n, Vs, order, sc);
+    *diag = As;
+    res = Vs;
+  } else {
+    sw = sym_eig(G, n, V, order, sc);
+    *diag = G;
+    res = V;
+  }
+  if (threadIdx.x == 0) {
+    sc.eig_calls += 1;
+    sc.eig_sweeps += sw;
+  }
+  tstop(sc, kPhEig, t0);
+  return res;
+}
+
+// ---------------------------------------------------------------------------
+// Block subspace iteration for the top-k left singular subspace of a tall
+// unfolding A (rows x cols, cols >= 2k), warm-started from the factor's current
+// value. Each iteration: Y = A^T U, B = Y^T Y (= U^T A A^T U), W = A Y; stop
+// when ||W - U B||_F <= 1e-13 ||B||_F (the subspace is then accurate to
+// ~1e-13 lambda_1 / gap); otherwise U = orth(W) by CholeskyQR2. A Rayleigh-Ritz
+// rotation by the eigenvectors of B then gives the exact top-k singular
+// vectors, identical (to rounding) to the SVD route of the reference. Returns
+// false — the caller falls back to Gram + Jacobi — when it does not converge in
+// kSiMaxIter iterations or CholeskyQR breaks down (rank deficiency, tiny gap).
+constexpr int kSiMaxIter = 40;
+// start of the subspace-iteration state in dynamic shared memory: after the
+// per-warp partial sums (nwarps x kSiMaxYK) and the Rayleigh-Ritz eigensolver
+// scratch (3 * 16^2)
+__device__ __forceinline__ constexpr int si_base() { return kWarps * 512; }
+constexpr int kSiMaxK = 16;     // register-tile bound on k
+constexpr int kSiMaxYK = 512;   // bound on cols * k (16 outputs per lane)
+
+// Warp 0 factors the SPD k x k matrix G = L L^T and writes Linv = L^{-1}
+// (both col-major, lower). Sets sc.ibcast[2] = 1 on a failed pivot.
+static __device__ void chol_inv_warp(const double* G, int k, double* L, double* Linv, BlockScratch& sc) {
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  double dmax = 0.0;
+  for (int j = 0; j < k; ++j) dmax = fmax(dmax, G[j + j * k]);
+  bool ok = dmax > 0.0;
+  for (int j = 0; j < k && ok; ++j) {
+    double sdiag = 0.0;
+    if (lane == j) {
+      sdiag = G[j + j * k];
+      for (int l = 0; l < j; ++l) sdiag -= L[j + l * k] * L[j + l * k];
+    }
+    sdiag = __shfl_sync(0xffffffffu, sdiag, j);
+    // A rank-deficient Gram has pivots ~eps*dmax; a basis with condition
+    // number <= ~1e7 keeps them >= 1e-14*dmax. Anything smaller falls back.
+    if (!(sdiag > 1e-14 * dmax)) {
+      ok = false;
+      break;
+    }
+    const double ljj = sqrt(sdiag), inv = 1.0 / ljj;
+    if (lane > j && lane < k) {
+      double v = G[lane + j * k];
+      for (int l = 0; l < j; ++l) v -= L[lane + l * k] * L[j + l * k];
+      L[lane + j * k] = v * inv;
+    }
+    if (lane == j) L[j + j * k] = ljj;
+    __syncwarp();
+  }
+  if (!ok) {
+    if (lane == 0) sc.ibcast[2] = 1;
+    return;
+  }
+  if (lane < k) {  // column `lane` of L^{-1} by forward substitution
+    const int c = lane;
+    for (int i = 0; i < c; ++i) Linv[i + c * k] = 0.0;
+    for (int i = c; i < k; ++i) {
+      double v = (i == c) ? 1.0 : 0.0;
+      for (int l = c; l < i; ++l) v -= L[i + l * k] * Linv[l + c * k];
+      Linv[i + c * k] = v / L[i + i * k];
+    }
+  }
+}
+
+// W (rows x K, ld rows) <- W L^{-T}, where W^T W = L L^T (one CholeskyQR pass).
+template <int K>
+__device__ __noinline__ bool cholqr_pass_k(double* W, int64_t rows, double* small, BlockScratch& sc) {
+  double* G = small;
+  double* L = small + K * K;
+  double* Li = small + 2 * K * K;
+  gram_tall(W, rows, rows, K, G);
+  if (threadIdx.x == 0) sc.ibcast[2] = 0;
+  __syncthreads();
+  chol_inv_warp(G, K, L, Li, sc);
+  __syncthreads();
+  if (sc.ibcast[2]) return false;
+  for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) {
+    double w[K];
+#pragma unroll
+    for (int l = 0; l < K; ++l) w[l] = W[r + l * rows];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      double v = 0.0;
+#pragma unroll
+      for (int l = 0; l <= j; ++l) v = fma(w[l], Li[j + l * K], v);
+      W[r + j * rows] = v;
+    }
+  }
+  __syncthreads();
+  return true;
+}
+
+// Y (cols x K) = A^T U with A(i, c) = P[offc[c] + i*inner]: warps split the
+// rows, each lane keeps up to 16 outputs in registers (row-outer loop, so the
+// loads of a row are independent), partials reduced through shared memory.
+template <int K>
+__device__ __noinline__ void unfold_At_U_k(const double* __restrict__ P, const int* __restrict__ offc, int64_t rows,
+                                           int64_t inner, int cols, const double* __restrict__ U,
+                                           double* __restrict__ Y, double* part) {
+  constexpr int OPL = 16;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = int(blockDim.x >> 5);
+  const int ne = cols * K;
+  const int64_t chunk = (rows + nw - 1) / nw;
+  const int64_t i0 = warp * chunk, i1 = imin(rows, i0 + chunk);
+  for (int e0 = 0; e0 < ne; e0 += 32 * OPL) {
+    double acc[OPL];
+    int oc[OPL], oj[OPL];
+#pragma unroll
+    for (int u = 0; u < OPL; ++u) {
+      const int e = e0 + lane + 32 * u;
+      const int ee = e < ne ? e : 0;
+      oc[u] = offc[ee % cols];
+      oj[u] = (ee / cols) * int(rows);
+      acc[u] = 0.0;
+    }
+    const int nu = imin(OPL, (ne - e0 - lane + 31) / 32);
+    for (int64_t i = i0; i < i1; ++i) {
+      const double* Pi = P + i * inner;
+      const double* Ui = U + i;
+#pragma unroll
+      for (int u = 0; u < OPL; ++u)
+        if (u < nu) acc[u] = fma(Pi[oc[u]], Ui[oj[u]], acc[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < OPL; ++u) {
+      const int e = e0 + lane + 32 * u;
+      if (u < nu && e < ne) part[warp * ne + e] = acc[u];
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+    double v = 0.0;
+    for (int w = 0; w < nw; ++w) v += part[w * ne + e];
+    Y[e] = v;  // e = c + j*cols: column-major cols x K
+  }
+  __syncthreads();
+}
+
+template <int K>
+__device__ __noinline__ int llsv_subspace_k(const double* P, int64_t outer, int64_t rows, int64_t inner, int kprev,
+                                            double* U, double* si, double* dsm, double* misc, BlockScratch& sc) {
+  const int cols = int(outer * inner);
+  // shared-memory carve-up: [0, si_base) partial sums / eigensolver scratch,
+  // then Y (cols x K), the small K x K matrices and the column-offset table
+  double* W = si;                          // rows x K (global workspace)
+  double* Y = dsm + si_base();             // cols x K   (<= 512)
+  double* small = Y + kSiMaxYK;            // 4 K x K
+  double* B = small + 4 * K * K;           // K x K
+  int* offc = reinterpret_cast<int*>(B + K * K);  // <= 512 ints
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) offc[c] = int((c / inner) * rows * inner + (c % inner));
+  if (kprev < K) {  // warm start padded with canonical vectors
+    for (int64_t idx = threadIdx.x; idx < rows * (K - kprev); idx += blockDim.x) {
+      const int64_t r = idx % rows, c = kprev + idx / rows;
+      U[r + c * rows] = (r == (c * 7919) % rows) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    if (!cholqr_pass_k<K>(U, rows, small, sc) || !cholqr_pass_k<K>(U, rows, small, sc)) return -1;
+  } else {
+    __syncthreads();
+  }
+  int iters = -1;
+  for (int it = 0; it < kSiMaxIter; ++it) {
+    long long tp = tstart();
+    unfold_At_U_k<K>(P, offc, rows, inner, cols, U, Y, dsm);
+    gram_tall(Y, cols, cols, K, B);
+    tstop(sc, kSiAtU, tp);
+    tp = tstart();
+    double rsq = 0.0;
+    for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+      double acc[K], u[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        acc[j] = 0.0;
+        u[j] = U[i + j * rows];
+      }
+      const double* Pi = P + i * inner;
+      for (int c = 0; c < cols; ++c) {
+        const double a = Pi[offc[c]];
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc[j] = fma(a, Y[c + j * cols], acc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        W[i + j * rows] = acc[j];
+        double v = acc[j];  // residual (W - U B)[i, j]
+#pragma unroll
+        for (int l = 0; l < K; ++l) v = fma(-u[l], B[l + j * K], v);
+        rsq = fma(v, v, rsq);
+      }
+    }
+    double bsq = 0.0;
+    for (int e = threadIdx.x; e < K * K; e += blockDim.x) bsq = fma(B[e], B[e], bsq);
+    rsq = block_sum(rsq, sc);
+    bsq = block_sum(bsq, sc);
+    tstop(sc, kSiAY, tp);
+    if (bsq > 0.0 && rsq <= 1e-26 * bsq) {
+      iters = it + 1;
+      break;
+    }
+    if (!(bsq > 0.0)) return -1;
+    tp = tstart();
+    if (!cholqr_pass_k<K>(W, rows, small, sc) || !cholqr_pass_k<K>(W, rows, small, sc)) return -1;
+    for (int64_t idx = threadIdx.x; idx < rows * K; idx += blockDim.x) U[idx] = W[idx];
+    __syncthreads();
+    tstop(sc, kSiQR, tp);
+  }
+  const long long trr = tstart();
+  if (iters < 0) return -1;
+  // Rayleigh-Ritz: U <- U R with B R = R diag(lambda), descending
+  int* order = reinterpret_cast<int*>(misc);
+  double* diag = nullptr;
+  const double* R = eig_run(B, K, small, order, dsm, &diag, sc);
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+    double u[K];
+#pragma unroll
+    for (int l = 0; l < K; ++l) u[l] = U[i + l * rows];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const double* rj = R + int64_t(order[j]) * K;
+      double v = 0.0;
+#pragma unroll
+      for (int l = 0; l < K; ++l) v = fma(u[l], rj[l], v);
+      W[i + j * rows] = v;
+    }
+  }
+  __syncthreads();
+  for (int64_t idx = threadIdx.x; idx < rows * K; idx += blockDim.x) U[idx] = W[idx];
+  __syncthreads();
+  sign_fix(U, rows, K, rows, nullptr, sc);
+  tstop(sc, kSiRR, trr);
+  return iters;
+}
+
+static __device__ bool llsv_subspace(const double* P, int64_t outer, int64_t rows, int64_t inner, int k, int kprev, double* U,
+                              double* si, double* dsm, double* misc, BlockScratch& sc) {
+  int it = -1;
+  switch (k) {
+#define TT_CASE(N) \
+  case N:          \
+    it = llsv_subspace_k<N>(P, outer, rows, inner, kprev, U, si, dsm, misc, sc); \
+    break;
+    TT_CASE(1) TT_CASE(2) TT_CASE(3) TT_CASE(4) TT_CASE(5) TT_CASE(6) TT_CASE(7) TT_CASE(8)
+    TT_CASE(9) TT_CASE(10) TT_CASE(11) TT_CASE(12) TT_CASE(13) TT_CASE(14) TT_CASE(15) TT_CASE(16)
+#undef TT_CASE
+    default:
+      break;
+  }
+  if (threadIdx.x == 0 && it > 0) sc.si_iters += it;
+  return it > 0;
+}
+
+// leading_left_singular_vectors (linalg.cpp:45-64) of the mode unfolding of a
+// row-major (outer, rows, inner) tensor, through the Gram matrix of its
+// smaller side. U: rows x k (ld rows), sign-fixed.
+static __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows, int64_t inner, int64_t k, double* U,
+                            double* G, double* V, double* misc, double* dsm, BlockScratch& sc, int64_t kprev = 0,
+                            double* si = nullptr) {
+  const int64_t cols = outer * inner;
+  if (si != nullptr && kprev > 0 && rows > cols && cols >= 2 * k && cols * k <= kSiMaxYK && k <= kSiMaxK &&
+      si_base() + kSiMaxYK + 5 * k * k + 256 <= sc.dsm_cap) {
+    const long long t0 = tstart();
+    const bool ok = llsv_subspace(P, outer, rows, inner, int(k), int(imin(kprev, k)), U, si, dsm, misc, sc);
+    tstop(sc, kPhEig, t0);
+    if (ok) {
+      if (threadIdx.x == 0) sc.si_ok += 1;
+      return;
+    }
+    if (threadIdx.x == 0) sc.si_fail += 1;
+  }
+  int* order = reinterpret_cast<int*>(misc);
+  double* sig = misc + kMisc / 2;
+  double* diag = nullptr;
+  if (rows <= cols) {
+    const int n = int(rows);
+    long long tg = tstart();
+    gram_rows(P, outer, rows, inner, G);
+    tstop(sc, kPhGram, tg);
+    const double* Vp = eig_run(G, n, V, order, dsm, &diag, sc);
+    for (int64_t idx = threadIdx.x; idx < rows * k; idx += blockDim.x) {
+      const int64_t i = idx % rows, c = idx / rows;
+      U[idx] = Vp[i + int64_t(order[c]) * n];
+    }
+    __syncthreads();
+  } else {
+    const int n = int(cols);
+    long long tg = tstart();
+    gram_cols(P, outer, rows, inner, G);
+    tstop(sc, kPhGram, tg);
+    const double* Vp = eig_run(G, n, V, order, dsm, &diag, sc);
+    if (threadIdx.x < k) {
+      const double l0 = fmax(diag[order[0] * (n + 1)], 0.0);
+      const double lc = fmax(diag[order[threadIdx.x] * (n + 1)], 0.0);
+      sig[threadIdx.x] = gram_sigma_ok(lc, l0) ? 1.0 / sqrt(lc) : 0.0;
+    }
+    __syncthreads();
+    tg = tstart();
+    for (int64_t idx = threadIdx.x; idx < rows * k; idx += blockDim.x) {
+      const int64_t i = idx % rows, c = idx / rows;
+      const double inv = sig[c];
+      double s = 0.0;
+      if (inv != 0.0) {
+        const double* vc = Vp + int64_t(order[c]) * n;
+        for (int64_t o = 0; o < outer; ++o) {
+          const double* a = P + (o * rows + i) * inner;
+          const double* v = vc + o * inner;
+          for (int64_t t = 0; t < inner; ++t) s = fma(a[t], v[t], s);
+        }
+      }
+      U[idx] = s * inv;
+    }
+    __syncthreads();
+    tstop(sc, kPhGram, tg);
+    const long long to = tstart();
+    orthonormalize(U, rows, 0, int(k), rows, sc);
+    tstop(sc, kPhOrtho, to);
+  }
+  const long long ts = tstart();
+  sign_fix(U, rows, int(k), rows, nullptr, sc);
+  tstop(sc, kPhOrtho, ts);
+}
+
+extern std::atomic<int64_t> g_launches;
+
+}  // namespace ttb
