@@ -149,6 +149,25 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int c0,
       : "memory");
 }
 
+// sum_k a[k*as] * b[k*bs] with four independent accumulators: the loads of
+// four iterations are issued back to back, so a runtime-length dot product
+// over L2-resident operands waits for one load latency per four terms.
+__device__ __forceinline__ double dot4(const double* __restrict__ a, int64_t as, const double* __restrict__ b,
+                                       int64_t bs, int64_t n) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int64_t k = 0;
+  for (; k + 3 < n; k += 4) {
+    const double a0 = a[k * as], a1 = a[(k + 1) * as], a2 = a[(k + 2) * as], a3 = a[(k + 3) * as];
+    const double b0 = b[k * bs], b1 = b[(k + 1) * bs], b2 = b[(k + 2) * bs], b3 = b[(k + 3) * bs];
+    s0 = fma(a0, b0, s0);
+    s1 = fma(a1, b1, s1);
+    s2 = fma(a2, b2, s2);
+    s3 = fma(a3, b3, s3);
+  }
+  for (; k < n; ++k) s0 = fma(a[k * as], b[k * bs], s0);
+  return (s0 + s1) + (s2 + s3);
+}
+
 // ---------------------------------------------------------------------------
 // Mode product on a row-major tensor viewed as (outer, d, inner):
 //   out[o][a][t] (+)= sum_j M(a, j) * in[o][j][t],  a < r,
@@ -213,9 +232,7 @@ __device__ __forceinline__ void gemm(int64_t M, int64_t N, int64_t K, const doub
       const int64_t k0 = part * kc, k1 = imin(K, k0 + kc);
       const double* a = A + i * ars;
       const double* b = B + j * bcs;
-      double s = 0.0;
-      for (int64_t k = k0; k < k1; ++k) s = fma(a[k * acs], b[k * brs], s);
-      sc.red[threadIdx.x] = s;
+      sc.red[threadIdx.x] = dot4(a + k0 * acs, acs, b + k0 * brs, brs, k1 - k0);
     }
     __syncthreads();
     if (threadIdx.x < tot) {
@@ -230,10 +247,7 @@ __device__ __forceinline__ void gemm(int64_t M, int64_t N, int64_t K, const doub
   }
   for (int64_t idx = threadIdx.x; idx < tot; idx += blockDim.x) {
     const int64_t i = idx % M, j = idx / M;
-    double s = 0.0;
-    const double* a = A + i * ars;
-    const double* b = B + j * bcs;
-    for (int64_t k = 0; k < K; ++k) s = fma(a[k * acs], b[k * brs], s);
+    const double s = dot4(A + i * ars, acs, B + j * bcs, brs, K);
     double* c = C + i * crs + j * ccs;
     *c = acc ? *c + s : s;
   }
@@ -293,7 +307,7 @@ __device__ __forceinline__ void gram_rows(const double* __restrict__ P, int64_t 
     for (int64_t o = 0; o < outer; ++o) {
       const double* pi = P + (o * rows + i) * inner;
       const double* pj = P + (o * rows + j) * inner;
-      for (int64_t t = 0; t < inner; ++t) s = fma(pi[t], pj[t], s);
+      s += dot4(pi, 1, pj, 1, inner);
     }
     G[i + j * rows] = s;
     G[j + i * rows] = s;
@@ -313,7 +327,7 @@ __device__ __forceinline__ void gram_cols(const double* __restrict__ P, int64_t 
     const double* p1 = P + o1 * rows * inner + t1;
     const double* p2 = P + o2 * rows * inner + t2;
     double s = 0.0;
-    for (int64_t i = 0; i < rows; ++i) s = fma(p1[i * inner], p2[i * inner], s);
+    s = dot4(p1, inner, p2, inner, rows);
     G[c1 + c2 * cols] = s;
     G[c2 + c1 * cols] = s;
   }

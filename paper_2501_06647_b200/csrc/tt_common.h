@@ -15,6 +15,9 @@
 namespace ttb {
 
 constexpr int kMaxP = 8;
+// Bound on the stacked temporal rows (sum of the parts' rho_0) of one stitch
+// (shared-memory row tables of the stitch kernel).
+constexpr int kStitchMaxRows = 1024;
 
 TT_HD int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
 TT_HD int64_t imax(int64_t a, int64_t b) { return a > b ? a : b; }

@@ -190,8 +190,7 @@ __device__ __forceinline__ void ttm_elems(const double* __restrict__ in, int64_t
     const int64_t a = q % r, o = q / r;
     const double* src = in + o * d * inner + t;
     const double* ma = M + a * ms_a;
-    double s = 0.0;
-    for (int64_t j = 0; j < d; ++j) s = fma(ma[j * ms_j], src[j * inner], s);
+    const double s = dot4(ma, ms_j, src, inner, d);
     out[e] = acc ? out[e] + s : s;
   }
   __syncthreads();
@@ -267,6 +266,15 @@ static __device__ double* eig_run(double* G, int n, double* V, int* order, doubl
 // false — the caller falls back to Gram + Jacobi — when it does not converge in
 // kSiMaxIter iterations or CholeskyQR breaks down (rank deficiency, tiny gap).
 constexpr int kSiMaxIter = 40;
+// subspace-iteration sub-phase timers; TT_PROBE_M0 hands the slots to the
+// stitch kernel's mode-0 solver instead (instrumented investigation builds)
+#ifdef TT_PROBE_M0
+__device__ __forceinline__ void tstop_si(BlockScratch&, int, long long) {}
+__device__ __forceinline__ void tstop_m0(BlockScratch& sc, int slot, long long t0) { tstop(sc, slot, t0); }
+#else
+__device__ __forceinline__ void tstop_si(BlockScratch& sc, int slot, long long t0) { tstop(sc, slot, t0); }
+__device__ __forceinline__ void tstop_m0(BlockScratch&, int, long long) {}
+#endif
 // start of the subspace-iteration state in dynamic shared memory: after the
 // per-warp partial sums (nwarps x kSiMaxYK) and the Rayleigh-Ritz eigensolver
 // scratch (3 * 16^2)
@@ -421,7 +429,7 @@ __device__ __noinline__ int llsv_subspace_k(const double* P, int64_t outer, int6
     long long tp = tstart();
     unfold_At_U_k<K>(P, offc, rows, inner, cols, U, Y, dsm);
     gram_tall(Y, cols, cols, K, B);
-    tstop(sc, kSiAtU, tp);
+    tstop_si(sc, kSiAtU, tp);
     tp = tstart();
     double rsq = 0.0;
     for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
@@ -450,7 +458,7 @@ __device__ __noinline__ int llsv_subspace_k(const double* P, int64_t outer, int6
     for (int e = threadIdx.x; e < K * K; e += blockDim.x) bsq = fma(B[e], B[e], bsq);
     rsq = block_sum(rsq, sc);
     bsq = block_sum(bsq, sc);
-    tstop(sc, kSiAY, tp);
+    tstop_si(sc, kSiAY, tp);
     if (bsq > 0.0 && rsq <= 1e-26 * bsq) {
       iters = it + 1;
       break;
@@ -460,7 +468,7 @@ __device__ __noinline__ int llsv_subspace_k(const double* P, int64_t outer, int6
     if (!cholqr_pass_k<K>(W, rows, small, sc) || !cholqr_pass_k<K>(W, rows, small, sc)) return -1;
     for (int64_t idx = threadIdx.x; idx < rows * K; idx += blockDim.x) U[idx] = W[idx];
     __syncthreads();
-    tstop(sc, kSiQR, tp);
+    tstop_si(sc, kSiQR, tp);
   }
   const long long trr = tstart();
   if (iters < 0) return -1;
@@ -485,7 +493,7 @@ __device__ __noinline__ int llsv_subspace_k(const double* P, int64_t outer, int6
   for (int64_t idx = threadIdx.x; idx < rows * K; idx += blockDim.x) U[idx] = W[idx];
   __syncthreads();
   sign_fix(U, rows, K, rows, nullptr, sc);
-  tstop(sc, kSiRR, trr);
+  tstop_si(sc, kSiRR, trr);
   return iters;
 }
 
@@ -531,7 +539,10 @@ static __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows,
   if (rows <= cols) {
     const int n = int(rows);
     long long tg = tstart();
-    gram_rows(P, outer, rows, inner, G);
+    if (inner == 1)  // A = P^T viewed (rows x outer): a GEMM with the K split across the block
+      gemm(rows, rows, outer, P, 1, rows, P, rows, 1, G, 1, rows, false, sc);
+    else
+      gram_rows(P, outer, rows, inner, G);
     tstop(sc, kPhGram, tg);
     const double* Vp = eig_run(G, n, V, order, dsm, &diag, sc);
     for (int64_t idx = threadIdx.x; idx < rows * k; idx += blockDim.x) {

@@ -382,6 +382,12 @@ std::vector<ProblemStatus> run_stitch_batch(Exec& ex, const Params& prm, std::ve
   const int n = static_cast<int>(descs_in.size());
   std::vector<ProblemStatus> st_out(static_cast<size_t>(n));
   if (n == 0) return st_out;
+  for (const StitchDesc& d : descs_in) {  // the kernel's shared-memory row tables
+    Index rows = 0;
+    for (int i = 0; i < d.nparts; ++i) rows += parts[size_t(d.part0) + i].rho[0];
+    if (rows > kStitchMaxRows)
+      fail(TT_EINVAL, "stitch: the parts' temporal ranks sum to more than " + std::to_string(kStitchMaxRows));
+  }
   // Launch longest-first: CTAs are dispatched roughly in index order and query
   // costs vary ~100x (L and the part count), so LPT order shrinks the tail.
   std::vector<int> perm(static_cast<size_t>(n));

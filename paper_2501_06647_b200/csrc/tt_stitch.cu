@@ -8,13 +8,14 @@
 namespace ttb {
 
 // ---------------------------------------------------------------------------
-// U_0 = blockdiag(V_sub,i) [E_i]  (L x K0, ld L), sign-fixed (linalg.cpp:15-31).
+// U_0 = blockdiag(V_sub,i) [E_i]  (L x K0, ld L), sign-fixed (linalg.cpp:15-31);
+// E_i = rows [roff[i], roff[i+1]) of the stacked E (ld R).
 // Pass 0 evaluates the rows without storing and finds each column's first
 // max-|.| row; pass 1 recomputes and stores U_0 once with the signs applied.
 // Two rows per thread are in flight, E_i is staged in shared memory.
 template <int K0>
-__device__ __noinline__ void materialize_u0_k(const StitchPart* __restrict__ parts, int s, const double* Ebase,
-                                              int64_t e_stride, double* __restrict__ U0, int64_t L, int* flips,
+__device__ __noinline__ void materialize_u0_k(const StitchPart* __restrict__ parts, int s, const double* Est,
+                                              int R, const int* roff, double* __restrict__ U0, int64_t L, int* flips,
                                               int64_t* idxbuf, double* Es, BlockScratch& sc) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const int nt = int(blockDim.x);
@@ -31,9 +32,9 @@ __device__ __noinline__ void materialize_u0_k(const StitchPart* __restrict__ par
     for (int i = 0; i < s; ++i) {
       const int64_t r0 = parts[i].rho[0], len = parts[i].len, ld = parts[i].ld0;
       const double* vs = parts[i].v0 + parts[i].row0;
-      const double* E = Ebase + int64_t(i) * e_stride;
+      const double* E = Est + roff[i];  // stacked E, ld R
       __syncthreads();
-      for (int64_t e = threadIdx.x; e < r0 * K0; e += nt) Es[e] = E[e];
+      for (int64_t e = threadIdx.x; e < r0 * K0; e += nt) Es[e] = E[(e % r0) + (e / r0) * R];
       __syncthreads();
       for (int64_t rb = threadIdx.x; rb < len; rb += 2 * nt) {
         const int64_t ra = rb, rc = rb + nt;
@@ -120,12 +121,12 @@ __device__ __noinline__ void materialize_u0_k(const StitchPart* __restrict__ par
   __syncthreads();
 }
 
-__device__ bool materialize_u0(int k0, const StitchPart* parts, int s, const double* Ebase, int64_t e_stride,
+__device__ bool materialize_u0(int k0, const StitchPart* parts, int s, const double* Est, int R, const int* roff,
                                double* U0, int64_t L, int* flips, int64_t* idxbuf, double* Es, BlockScratch& sc) {
   switch (k0) {
 #define TT_CASE(N) \
   case N:          \
-    materialize_u0_k<N>(parts, s, Ebase, e_stride, U0, L, flips, idxbuf, Es, sc); \
+    materialize_u0_k<N>(parts, s, Est, R, roff, U0, L, flips, idxbuf, Es, sc); \
     return true;
     TT_CASE(1) TT_CASE(2) TT_CASE(3) TT_CASE(4) TT_CASE(5) TT_CASE(6) TT_CASE(7) TT_CASE(8)
     TT_CASE(9) TT_CASE(10) TT_CASE(11) TT_CASE(12) TT_CASE(13) TT_CASE(14) TT_CASE(15) TT_CASE(16)
@@ -227,33 +228,27 @@ __device__ __forceinline__ void gemm_batched(int n, Gen gen, BlockScratch& sc) {
       const int o = int(q / g.M);
       const double* __restrict__ a = g.A + int64_t(o) * g.aos + int64_t(ii) * g.ars;
       const double* __restrict__ b = g.B + int64_t(o) * g.bos + int64_t(jj) * g.bcs;
-      double s0 = 0.0, s1 = 0.0;
-      int kk = 0;
-      for (; kk + 1 < g.K; kk += 2) {
-        s0 = fma(a[int64_t(kk) * g.acs], b[int64_t(kk) * g.brs], s0);
-        s1 = fma(a[int64_t(kk + 1) * g.acs], b[int64_t(kk + 1) * g.brs], s1);
-      }
-      if (kk < g.K) s0 = fma(a[int64_t(kk) * g.acs], b[int64_t(kk) * g.brs], s0);
+      const double sum = dot4(a, g.acs, b, g.brs, g.K);
       double* c = g.C + int64_t(o) * g.cos + int64_t(ii) * g.crs + int64_t(jj) * g.ccs;
-      *c = g.acc ? *c + (s0 + s1) : (s0 + s1);
+      *c = g.acc ? *c + sum : sum;
     }
   }
   __syncthreads();
   tstop(sc, kPhTtm, t0);
 }
 
-// Stacked temporal rows of all parts (mode-0 coordinates): row r of the
-// stacked E / A / C matrices belongs to part rt_part[r], local row rt_loc[r];
-// rt_ld[r] = the part's rho_0 (negated for a partial hit, whose rows carry the
-// metric S_i).
-constexpr int kRowTab = 512;
+// Stacked temporal rows of all parts (mode-0 coordinates): part i owns rows
+// [roff[i], roff[i+1]) of the stacked E / A / C matrices (R = sum rho_i0 rows);
+// rt_pp[r] = the part of row r if it is a partial hit (rows carrying the
+// metric S_i), else -1. The host rejects stitches with more rows.
+constexpr int kRowTab = kStitchMaxRows;
 
 __global__ void __launch_bounds__(kStitchThreads, kStitchCtas)
     stitch_als_kernel(Params prm, const StitchDesc* __restrict__ descs, const StitchPart* __restrict__ parts_all) {
   __shared__ BlockScratch sc;
   __shared__ int flips[kMaxVec];
   __shared__ int64_t idxbuf[kWarps * kMaxVec];
-  __shared__ int rt_part[kRowTab], rt_loc[kRowTab], rt_ld[kRowTab];
+  __shared__ int roff[kRowTab + 1], rt_pp[kRowTab];
   extern __shared__ double dsm[];
   const long long t_kernel = tstart();
   if (threadIdx.x == 0) {
@@ -286,12 +281,35 @@ __global__ void __launch_bounds__(kStitchThreads, kStitchCtas)
     for (int q = 1; q < m; ++q) off += rc[q] * rcx[q];
     return ws + lay.P + int64_t(i) * lay.per_part_P + off;
   };
-  auto Cp = [&](int i) { return ws + lay.C + int64_t(i) * lay.per_part_C; };
+
   auto Sp = [&](int i) { return ws + lay.S + int64_t(i) * lay.per_part_S; };
-  auto Ep = [&](int i) { return ws + lay.E + int64_t(i) * lay.per_part_E; };
-  auto Ap = [&](int i) { return ws + lay.A + int64_t(i) * lay.per_part_E; };
-  auto E2p = [&](int i) { return ws + lay.E2 + int64_t(i) * lay.per_part_E; };
   double* TB[2] = {ws + lay.TB1, ws + lay.TB2};  // part-batched chain scratch, stride lay.chain
+  // stacked temporal rows: part i owns rows [roff[i], roff[i+1])
+  int R = 0;
+  bool any_partial = false;
+  for (int i = 0; i < s; ++i) {
+    R += int(parts[i].rho[0]);
+    any_partial = any_partial || parts[i].partial;
+  }
+  if (threadIdx.x == 0) {
+    int o = 0;
+    for (int i = 0; i < s; ++i) {
+      roff[i] = o;
+      o += int(parts[i].rho[0]);
+    }
+    roff[s] = o;
+  }
+  __syncthreads();
+  for (int i = 0; i < s; ++i) {
+    const int pp = parts[i].partial ? i : -1;
+    for (int r = roff[i] + threadIdx.x; r < roff[i + 1]; r += blockDim.x) rt_pp[r] = pp;
+  }
+  __syncthreads();
+  double* Est = ws + lay.E;  // stacked E (R x k0, ld R): U0 = blockdiag(V_sub,i) E
+  double* Ast = ws + lay.A;  // stacked A = S E (rows of partial parts)
+  double* Cst = ws + lay.C;  // stacked C (R x Q, row-major)
+  auto Ep = [&](int i) { return Est + roff[i]; };  // ld R
+  auto Ap = [&](int i) { return Ast + roff[i]; };  // ld R
 
   // ---- partial-hit metric S_i = Vsub^T Vsub and the norm of the implied tensor
   double norm_sq = 0.0;
@@ -356,35 +374,13 @@ __global__ void __launch_bounds__(kStitchThreads, kStitchCtas)
       return g;
     };
     gemm_batched(s * (p - 1), [&](int e) { return pm_entry(e / (p - 1), 1 + e % (p - 1)); }, sc);
-    // stacked temporal-row table for the part-batched mode-0 solver
-    int64_t rows_total = 0;
-    bool any_partial = false;
-    for (int i = 0; i < s; ++i) {
-      rows_total += parts[i].rho[0];
-      any_partial = any_partial || parts[i].partial;
-    }
-    if (rows_total <= kRowTab) {
-      if (threadIdx.x < 32) {
-        int r = 0;
-        for (int i = 0; i < s; ++i) {
-          const int r0 = int(parts[i].rho[0]);
-          const int ld = parts[i].partial ? -r0 : r0;
-          for (int a = threadIdx.x; a < r0; a += 32) {
-            rt_part[r + a] = i;
-            rt_loc[r + a] = a;
-            rt_ld[r + a] = ld;
-          }
-          r += r0;
-        }
-      }
-      __syncthreads();
-    }
     const double norm = sqrt(norm_sq);
     double prev_fit = nan("");
     for (int sweep = 0; sweep < prm.max_iters; ++sweep) {
       // ================= mode 0 (stitch_temporal_unfolding, stitch.cpp:49-73)
       const int64_t k0n = stitch_mode_rank(p, d, rc, k, 0);
       const int64_t Q = prod_range(k, 1, p);
+      auto Cp = [&](int i) { return Cst + int64_t(roff[i]) * Q; };  // rows of part i (row-major, stride Q)
       // C_i = M0(H_i x_{p-1} P_{i,p-1} ... x_1 P_i1), descending as the reference;
       // one batched pass per mode over all parts
       for (int m = p - 1; m >= 1; --m) {
@@ -393,7 +389,7 @@ __global__ void __launch_bounds__(kStitchThreads, kStitchCtas)
           int64_t cur[kMaxP];
           for (int q = 0; q < p; ++q) cur[q] = q > m ? k[q] : parts[i].rho[q];
           const double* src = step == 0 ? parts[i].core : TB[(step - 1) & 1] + int64_t(i) * lay.chain;
-          double* dst = (m == 1) ? Cp(i) : TB[step & 1] + int64_t(i) * lay.chain;
+          double* dst = (m == 1) ? Cst + int64_t(roff[i]) * Q : TB[step & 1] + int64_t(i) * lay.chain;
           return bg_mode_product(src, prod_range(cur, 0, m), cur[m], prod_range(cur, m + 1, p), Pm(i, m), 1, k[m],
                                  k[m], dst);
         }, sc);
@@ -403,98 +399,80 @@ __global__ void __launch_bounds__(kStitchThreads, kStitchCtas)
       // E <- C (C^T S E). Warm start: the previous sweep's E, or in sweep 0 the
       // k0 columns of C with the largest S-norm. Rayleigh-Ritz makes E the exact
       // left singular vectors; any failure falls through to the eigen paths.
-      // All parts are processed together: E, A = S E and C are handled as
-      // stacked (sum rho_i0)-row matrices through the row table, so an
-      // iteration costs a fixed number of block passes whatever s is.
+      // All parts are processed together as stacked R-row matrices (E, A = S E
+      // in shared memory, C row-major in the workspace), so an iteration costs
+      // a fixed number of block passes whatever s is.
       bool mode0_done = false;
-      int64_t rho0_sum = 0;
-      for (int i = 0; i < s; ++i) rho0_sum += parts[i].rho[0];
-      if (k0n <= kSiMaxK && Q >= 2 * k0n && Q * k0n <= kSiMaxYK && rho0_sum >= k0n && rho0_sum <= kRowTab &&
-          rho0_sum * k0n <= si_base()) {
+      const int kk = int(k0n);
+      constexpr int kSiE = 2560;  // shared-memory offset of E (below: eig scratch, Y, small matrices)
+      if (kk <= kSiMaxK && Q >= 2 * kk && Q * kk <= kSiMaxYK && R >= kk && kSiE + 2 * R * kk <= sc.dsm_cap) {
         const long long t_si = tstart();
-        const int kk = int(k0n);
-        const int R = int(rho0_sum);
         const int nt = int(blockDim.x);
-        double* As = dsm;                             // R x kk stacked A = S E (ld R)
-        double* Y = dsm + si_base();                  // Q x kk
-        double* small = Y + kSiMaxYK;                 // G, L, Linv (k x k each)
-        double* B = small + 4 * kk * kk;              // k x k
-        double* Eg = ws + lay.E;
-        double* E2g = ws + lay.E2;
-        double* Rg = Z;                               // residual, per-part layout of E
-        const int64_t ppE = lay.per_part_E, ppC = lay.per_part_C;
-        // element (r, j) of a per-part E-layout matrix
-        auto eoff = [&](int r, int j) -> int64_t {
-          const int ld = rt_ld[r] < 0 ? -rt_ld[r] : rt_ld[r];
-          return int64_t(rt_part[r]) * ppE + rt_loc[r] + int64_t(j) * ld;
-        };
-        // dst = S src for every stacked row (entire parts: S = I); to the stacked
-        // shared-memory A, or to the per-part global A (Ap) when `global`
-        auto apply_S_all = [&](const double* src, bool global) {
+        const int Qi = int(Q);
+        double* Y = dsm + 768;            // Q x kk
+        double* small = dsm + 1280;       // G, L, Linv (kk x kk each)
+        double* B = small + 4 * kk * kk;  // kk x kk
+        double* Es = dsm + kSiE;          // R x kk (ld R)
+        double* As = Es + R * kk;         // R x kk (ld R)
+        double* Rg = Z;                   // residual rows of partial parts (ld R)
+        // dst = S src (entire rows: S = I); both stacked, ld R
+        auto apply_S_all = [&](const double* src, double* dst) {
           for (int idx = threadIdx.x; idx < R * kk; idx += nt) {
             const int r = idx % R, j = idx / R;
-            const int ldr = rt_ld[r];
+            const int i = rt_pp[r];
             double v;
-            if (ldr < 0) {
-              const int r0 = -ldr, a = rt_loc[r], i = rt_part[r];
-              const double* S = Sp(i) + a;
-              const double* e = src + int64_t(i) * ppE + int64_t(j) * r0;
+            if (i < 0) {
+              v = src[idx];
+            } else {
+              const int o = roff[i], r0 = roff[i + 1] - o;
+              const double* S = Sp(i) + (r - o);
+              const double* e = src + o + j * R;
               v = 0.0;
               for (int b = 0; b < r0; ++b) v = fma(S[b * r0], e[b], v);
-            } else {
-              v = src[eoff(r, j)];
             }
-            if (global) {
-              (ws + lay.A)[eoff(r, j)] = v;
-            } else {
-              As[r + j * R] = v;
-            }
+            dst[idx] = v;
           }
           __syncthreads();
         };
-        // G (k x k, smem) = src^T As  (K = R split across the block)
-        auto gram_EA = [&](const double* src, double* Gk) {
+        // S-orthonormalise Es in place (two CholeskyQR passes in the metric S)
+        auto s_orth = [&]() -> bool {
           const int tot = kk * kk;
           const int nsplit = nt / tot > 0 ? nt / tot : 1;
-          if (threadIdx.x < tot * nsplit) {
-            const int e = threadIdx.x % tot, part = threadIdx.x / tot;
-            const int j1 = e % kk, j2 = e / kk;
-            double v = 0.0;
-            for (int r = part; r < R; r += nsplit) v = fma(src[eoff(r, j1)], As[r + j2 * R], v);
-            sc.red[threadIdx.x] = v;
-          }
-          __syncthreads();
-          if (threadIdx.x < tot) {
-            double v = 0.0;
-            for (int part = 0; part < nsplit; ++part) v += sc.red[part * tot + threadIdx.x];
-            Gk[threadIdx.x] = v;
-          }
-          __syncthreads();
-        };
-        // S-orthonormalise: E = src orthonormalised in the metric S (two CholeskyQR passes)
-        auto s_orth = [&](const double* src) -> bool {
+          double* Gk = small;
+          double* Li = small + 2 * kk * kk;
           for (int pass = 0; pass < 2; ++pass) {
-            const double* in = pass == 0 ? src : Eg;
-            double* Gk = small;
-            double* Lk = small + kk * kk;
-            double* Li = small + 2 * kk * kk;
-            apply_S_all(in, false);
-            gram_EA(in, Gk);
+            apply_S_all(Es, As);
+            if (threadIdx.x < tot * nsplit) {  // G = E^T A, rows split across the block
+              const int e = threadIdx.x % tot, part = threadIdx.x / tot;
+              const double* x = Es + (e % kk) * R;
+              const double* y = As + (e / kk) * R;
+              double v = 0.0;
+              for (int r = part; r < R; r += nsplit) v = fma(x[r], y[r], v);
+              sc.red[threadIdx.x] = v;
+            }
             if (threadIdx.x == 0) sc.ibcast[2] = 0;
             __syncthreads();
-            chol_inv_warp(Gk, kk, Lk, Li, sc);
+            if (threadIdx.x < tot) {
+              double v = 0.0;
+              for (int part = 0; part < nsplit; ++part) v += sc.red[part * tot + threadIdx.x];
+              Gk[threadIdx.x] = v;
+            }
+            __syncthreads();
+            chol_inv_warp(Gk, kk, small + tot, Li, sc);
             __syncthreads();
             if (sc.ibcast[2]) return false;
             for (int r = threadIdx.x; r < R; r += nt) {
               double w[kSiMaxK];
 #pragma unroll
-              for (int l = 0; l < kSiMaxK; ++l) w[l] = l < kk ? in[eoff(r, l)] : 0.0;
-              for (int j = 0; j < kk; ++j) {
-                double v = 0.0;
+              for (int l = 0; l < kSiMaxK; ++l) w[l] = l < kk ? Es[r + l * R] : 0.0;
 #pragma unroll
-                for (int l = 0; l < kSiMaxK; ++l)
-                  if (l <= j) v = fma(w[l], Li[j + l * kk], v);
-                Eg[eoff(r, j)] = v;
+              for (int j = 0; j < kSiMaxK; ++j) {
+                if (j < kk) {
+                  double v = 0.0;
+#pragma unroll
+                  for (int l = 0; l <= j; ++l) v = fma(w[l], Li[j + l * kk], v);
+                  Es[r + j * R] = v;
+                }
               }
             }
             __syncthreads();
@@ -502,102 +480,131 @@ __global__ void __launch_bounds__(kStitchThreads, kStitchCtas)
           return true;
         };
         bool ok = true;
+        long long tp = tstart();
         if (sweep == 0 || k[0] < k0n) {
           // start: the k0 columns of C with the largest S-norm
           double* cn = misc + kMisc / 2;  // Q norms
-          for (int64_t j = threadIdx.x; j < Q; j += nt) {
+          for (int q = threadIdx.x; q < Qi; q += nt) {
             double v = 0.0;
             for (int i = 0; i < s; ++i) {
-              const int64_t r0 = parts[i].rho[0];
-              const double* Ci = Cp(i);
+              const int o = roff[i], r0 = roff[i + 1] - o;
+              const double* Ci = Cst + int64_t(o) * Qi + q;
               if (parts[i].partial) {
                 const double* S = Sp(i);
-                for (int64_t a = 0; a < r0; ++a)
-                  for (int64_t b = 0; b < r0; ++b) v = fma(Ci[a * Q + j] * S[a + b * r0], Ci[b * Q + j], v);
+                for (int a = 0; a < r0; ++a)
+                  for (int b = 0; b < r0; ++b) v = fma(Ci[a * Qi] * S[a + b * r0], Ci[b * Qi], v);
               } else {
-                for (int64_t a = 0; a < r0; ++a) v = fma(Ci[a * Q + j], Ci[a * Q + j], v);
+                for (int a = 0; a < r0; ++a) v = fma(Ci[a * Qi], Ci[a * Qi], v);
               }
             }
-            cn[j] = v;
+            cn[q] = v;
           }
           __syncthreads();
           int* pick = reinterpret_cast<int*>(misc);
-          for (int64_t j = threadIdx.x; j < Q; j += nt) {
+          for (int q = threadIdx.x; q < Qi; q += nt) {
             int rank = 0;
-            for (int64_t l = 0; l < Q; ++l) rank += (cn[l] > cn[j] || (cn[l] == cn[j] && l < j));
-            if (rank < kk) pick[rank] = int(j);
+            for (int l = 0; l < Qi; ++l) rank += (cn[l] > cn[q] || (cn[l] == cn[q] && l < q));
+            if (rank < kk) pick[rank] = q;
           }
           __syncthreads();
           for (int idx = threadIdx.x; idx < R * kk; idx += nt) {
             const int r = idx % R, c = idx / R;
-            E2g[eoff(r, c)] = ws[lay.C + int64_t(rt_part[r]) * ppC + int64_t(rt_loc[r]) * Q + pick[c]];
+            Es[idx] = Cst[int64_t(r) * Qi + pick[c]];
           }
           __syncthreads();
-          ok = s_orth(E2g);
-        } else if (k[0] > k0n) {
-          // previous E has more columns (ld rho0): keep the first k0n (same ld)
-          ok = true;
+          ok = s_orth();
+        } else {
+          // warm start: the previous sweep's E (first k0n columns, ld R)
+          for (int idx = threadIdx.x; idx < R * kk; idx += nt) Es[idx] = Est[idx];
+          __syncthreads();
         }
+        tstop_m0(sc, kSiAtU, tp);
         bool conv = false;
         for (int it = 0; ok && it < kSiMaxIter; ++it) {
           // A = S E ; Y = C^T A (Q x k) ; B = Y^T Y ; W = C Y
-          apply_S_all(Eg, false);
-          for (int idx = threadIdx.x; idx < Q * kk; idx += nt) {
-            const int q = idx % int(Q), j = idx / int(Q);
-            const double* Aj = As + j * R;
-            double v0 = 0.0, v1 = 0.0;
+          tp = tstart();
+          apply_S_all(Es, As);
+          for (int idx = threadIdx.x; idx < Qi * kk; idx += nt) {
+            const int q = idx % Qi, j = idx / Qi;
+            const double* a = As + j * R;
+            const double* c = Cst + q;
+            double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
             int r = 0;
-            for (; r + 1 < R; r += 2) {
-              v0 = fma(ws[lay.C + int64_t(rt_part[r]) * ppC + int64_t(rt_loc[r]) * Q + q], Aj[r], v0);
-              v1 = fma(ws[lay.C + int64_t(rt_part[r + 1]) * ppC + int64_t(rt_loc[r + 1]) * Q + q], Aj[r + 1], v1);
+            for (; r + 3 < R; r += 4) {
+              v0 = fma(c[int64_t(r) * Qi], a[r], v0);
+              v1 = fma(c[int64_t(r + 1) * Qi], a[r + 1], v1);
+              v2 = fma(c[int64_t(r + 2) * Qi], a[r + 2], v2);
+              v3 = fma(c[int64_t(r + 3) * Qi], a[r + 3], v3);
             }
-            if (r < R) v0 = fma(ws[lay.C + int64_t(rt_part[r]) * ppC + int64_t(rt_loc[r]) * Q + q], Aj[r], v0);
-            Y[idx] = v0 + v1;
+            for (; r < R; ++r) v0 = fma(c[int64_t(r) * Qi], a[r], v0);
+            Y[idx] = (v0 + v1) + (v2 + v3);
           }
           __syncthreads();
-          {
-            const int tot = kk * kk;
-            for (int e = threadIdx.x; e < tot; e += nt) {
-              const int j1 = e % kk, j2 = e / kk;
-              double v = 0.0;
-              for (int q = 0; q < int(Q); ++q) v = fma(Y[q + j1 * Q], Y[q + j2 * Q], v);
-              B[e] = v;
-            }
-            __syncthreads();
+          for (int e = threadIdx.x; e < kk * kk; e += nt) {
+            const double* y1 = Y + (e % kk) * Qi;
+            const double* y2 = Y + (e / kk) * Qi;
+            double v = 0.0;
+            for (int q = 0; q < Qi; ++q) v = fma(y1[q], y2[q], v);
+            B[e] = v;
           }
-          // W = C Y (into E2), residual Rres = W - E B; rsq = <Rres, S Rres>
+          __syncthreads();
+          tstop_m0(sc, kSiAY, tp);
+          tp = tstart();
+          // per row: W = C Y (into As), residual W - E B: rsq += |.|^2 on entire
+          // rows, partial rows keep it for the metric term
           double rsq = 0.0;
-          for (int idx = threadIdx.x; idx < R * kk; idx += nt) {
-            const int r = idx % R, j = idx / R;
-            const double* Cr = ws + lay.C + int64_t(rt_part[r]) * ppC + int64_t(rt_loc[r]) * Q;
-            const double* Yj = Y + int64_t(j) * Q;
-            double w0 = 0.0, w1 = 0.0;
-            int q = 0;
-            for (; q + 1 < int(Q); q += 2) {
-              w0 = fma(Cr[q], Yj[q], w0);
-              w1 = fma(Cr[q + 1], Yj[q + 1], w1);
+          for (int r = threadIdx.x; r < R; r += nt) {
+            double w[kSiMaxK], e[kSiMaxK];
+#pragma unroll
+            for (int l = 0; l < kSiMaxK; ++l) {
+              w[l] = 0.0;
+              e[l] = l < kk ? Es[r + l * R] : 0.0;
             }
-            if (q < int(Q)) w0 = fma(Cr[q], Yj[q], w0);
-            const double w = w0 + w1;
-            double v = w;
-            for (int l = 0; l < kk; ++l) v = fma(-Eg[eoff(r, l)], B[l + j * kk], v);
-            const int64_t o = eoff(r, j);
-            E2g[o] = w;
-            Rg[o] = v;
-            if (rt_ld[r] > 0) rsq = fma(v, v, rsq);
+            const double* Cr = Cst + int64_t(r) * Qi;
+            int q = 0;
+            for (; q + 3 < Qi; q += 4) {  // four C loads in flight
+              const double c0 = Cr[q], c1 = Cr[q + 1], c2 = Cr[q + 2], c3 = Cr[q + 3];
+#pragma unroll
+              for (int l = 0; l < kSiMaxK; ++l)
+                if (l < kk) {
+                  const double* y = Y + q + l * Qi;
+                  w[l] = fma(c3, y[3], fma(c2, y[2], fma(c1, y[1], fma(c0, y[0], w[l]))));
+                }
+            }
+            for (; q < Qi; ++q) {
+              const double cv = Cr[q];
+#pragma unroll
+              for (int l = 0; l < kSiMaxK; ++l)
+                if (l < kk) w[l] = fma(cv, Y[q + l * Qi], w[l]);
+            }
+            const bool part_row = rt_pp[r] >= 0;
+#pragma unroll
+            for (int j = 0; j < kSiMaxK; ++j) {
+              if (j < kk) {
+                double v = w[j];
+#pragma unroll
+                for (int l = 0; l < kSiMaxK; ++l)
+                  if (l < kk) v = fma(-e[l], B[l + j * kk], v);
+                As[r + j * R] = w[j];
+                if (part_row)
+                  Rg[r + j * R] = v;
+                else
+                  rsq = fma(v, v, rsq);
+              }
+            }
           }
           __syncthreads();
           if (any_partial) {
             for (int idx = threadIdx.x; idx < R * kk; idx += nt) {
               const int r = idx % R, j = idx / R;
-              const int ldr = rt_ld[r];
-              if (ldr >= 0) continue;
-              const int r0 = -ldr, a = rt_loc[r], i = rt_part[r];
-              const double* S = Sp(i) + a;
-              const double* e = Rg + int64_t(i) * ppE + int64_t(j) * r0;
+              const int i = rt_pp[r];
+              if (i < 0) continue;
+              const int o = roff[i], r0 = roff[i + 1] - o;
+              const double* S = Sp(i) + (r - o);
+              const double* e = Rg + o + j * R;
               double v = 0.0;
               for (int b = 0; b < r0; ++b) v = fma(S[b * r0], e[b], v);
-              rsq = fma(v, e[a], rsq);
+              rsq = fma(v, Rg[idx], rsq);
             }
           }
           double bsq = 0.0;
@@ -613,28 +620,38 @@ __global__ void __launch_bounds__(kStitchThreads, kStitchCtas)
             if (threadIdx.x == 0) sc.si_iters += it + 1;
             break;
           }
-          ok = s_orth(E2g);
+          tstop_m0(sc, kSiQR, tp);
+          tp = tstart();
+          for (int idx = threadIdx.x; idx < R * kk; idx += nt) Es[idx] = As[idx];
+          __syncthreads();
+          ok = s_orth();
+          tstop_m0(sc, kSiRR, tp);
         }
         if (ok && conv) {
-          // Rayleigh-Ritz: E <- E R (descending), then A_i = S_i E_i
+          // Rayleigh-Ritz: E <- E R (descending); store E and A = S E
           int* order = reinterpret_cast<int*>(misc);
           double* diag = nullptr;
           const double* Rv = eig_run(B, kk, small, order, dsm, &diag, sc);
           for (int r = threadIdx.x; r < R; r += nt) {
             double w[kSiMaxK];
 #pragma unroll
-            for (int l = 0; l < kSiMaxK; ++l) w[l] = l < kk ? Eg[eoff(r, l)] : 0.0;
+            for (int l = 0; l < kSiMaxK; ++l) w[l] = l < kk ? Es[r + l * R] : 0.0;
             for (int j = 0; j < kk; ++j) {
-              const double* rj = Rv + int64_t(order[j]) * kk;
+              const double* rj = Rv + order[j] * kk;
               double v = 0.0;
 #pragma unroll
               for (int l = 0; l < kSiMaxK; ++l)
                 if (l < kk) v = fma(w[l], rj[l], v);
-              Eg[eoff(r, j)] = v;
+              Est[r + j * R] = v;
+              Es[r + j * R] = v;
             }
           }
           __syncthreads();
-          if (any_partial) apply_S_all(Eg, true);
+          if (any_partial) {
+            apply_S_all(Es, As);
+            for (int idx = threadIdx.x; idx < R * kk; idx += nt) Ast[idx] = As[idx];
+            __syncthreads();
+          }
           any_zero_sigma = 0;
           mode0_done = true;
           if (threadIdx.x == 0) sc.si_ok += 1;
@@ -644,53 +661,29 @@ __global__ void __launch_bounds__(kStitchThreads, kStitchCtas)
         tstop(sc, kPhEig, t_si);
       }
       // Row-compressed variant: with entire parts only, Z0 = blockdiag(V_i0) C
-      // (C = [C_1; ...; C_s], sum rho_i0 rows) and V_i0 orthonormal, so the left
-      // singular vectors of Z0 are blockdiag(V_i0) times the eigenvectors of
-      // C C^T — a (sum rho_i0)^2 problem instead of Q^2 when that is smaller
-      // (every two-part append stitch), with no Sigma^-1 amplification.
-      int64_t rsum = 0;
-      bool all_entire = true;
-      for (int i = 0; i < s; ++i) {
-        rsum += parts[i].rho[0];
-        all_entire = all_entire && !parts[i].partial;
-      }
+      // (C = [C_1; ...; C_s], R = sum rho_i0 rows) and V_i0 orthonormal, so the
+      // left singular vectors of Z0 are blockdiag(V_i0) times the eigenvectors
+      // of C C^T — an R^2 problem instead of Q^2 when that is smaller, with no
+      // Sigma^-1 amplification.
       if (mode0_done) {
-        // E_i, A_i already set by the subspace iteration
-      } else if (all_entire && rsum < Q && k0n <= rsum) {  // else: rank-deficient Z0 needs the completion path
-        int64_t oi = 0;
-        for (int i = 0; i < s; ++i) {
-          const int64_t ri = parts[i].rho[0];
-          int64_t oj = 0;
-          for (int j = 0; j < s; ++j) {
-            const int64_t rj = parts[j].rho[0];
-            // H[oi.., oj..] = C_i C_j^T
-            tgemm(ri, rj, Q, Cp(i), Q, 1, Cp(j), 1, Q, G + oi + oj * rsum, 1, rsum, false, sc);
-            oj += rj;
-          }
-          oi += ri;
-        }
+        // E, A already set by the subspace iteration
+      } else if (!any_partial && R < Q && k0n <= R) {  // else: rank-deficient Z0 needs the completion path
+        tgemm(R, R, Q, Cst, Q, 1, Cst, 1, Q, G, 1, R, false, sc);
         int* order = reinterpret_cast<int*>(misc);
         double* diag = nullptr;
-        const double* Vp = eig_run(G, int(rsum), Vg, order, dsm, &diag, sc);
-        oi = 0;
-        for (int i = 0; i < s; ++i) {
-          const int64_t ri = parts[i].rho[0];
-          double* E = Ep(i);
-          for (int64_t idx = threadIdx.x; idx < ri * k0n; idx += blockDim.x) {
-            const int64_t a = idx % ri, c = idx / ri;
-            E[idx] = Vp[oi + a + int64_t(order[c]) * rsum];
-          }
-          oi += ri;
+        const double* Vp = eig_run(G, R, Vg, order, dsm, &diag, sc);
+        for (int64_t idx = threadIdx.x; idx < int64_t(R) * k0n; idx += blockDim.x) {
+          const int64_t r = idx % R, c = idx / R;
+          Est[idx] = Vp[r + int64_t(order[c]) * R];
         }
         __syncthreads();
         any_zero_sigma = 0;
       } else {
         // G0 = Z0^T Z0 = sum_i C_i^T S_i C_i   (Q x Q)
         for (int i = 0; i < s; ++i) {
-          const PartView pv = load_part(parts[i]);
-          const int64_t r0 = pv.rho[0];
+          const int64_t r0 = parts[i].rho[0];
           const double* rhs = Cp(i);
-          if (pv.partial) {
+          if (parts[i].partial) {
             tgemm(r0, Q, r0, Sp(i), 1, r0, Cp(i), Q, 1, T[0], Q, 1, false, sc);
             rhs = T[0];
           }
@@ -717,13 +710,13 @@ __global__ void __launch_bounds__(kStitchThreads, kStitchCtas)
           __syncthreads();
           any_zero_sigma = sc.ibcast[1];
         }
-        // E_i = C_i W Sigma^-1 (rho0 x k0);  A_i = S_i E_i = (U0[rows_i]^T V_i0)^T
-        for (int i = 0; i < s; ++i) {
-          const PartView pv = load_part(parts[i]);
-          const int64_t r0 = pv.rho[0];
-          tgemm(r0, k0n, Q, Cp(i), Q, 1, wk, 1, Q, Ep(i), 1, r0, false, sc);
-          if (pv.partial) tgemm(r0, k0n, r0, Sp(i), 1, r0, Ep(i), 1, r0, Ap(i), 1, r0, false, sc);
-        }
+        // E = C W Sigma^-1 (R x k0, stacked);  A_i = S_i E_i = (U0[rows_i]^T V_i0)^T
+        tgemm(R, k0n, Q, Cst, Q, 1, wk, 1, Q, Est, 1, R, false, sc);
+        for (int i = 0; i < s; ++i)
+          if (parts[i].partial) {
+            const int64_t r0 = parts[i].rho[0];
+            tgemm(r0, k0n, r0, Sp(i), 1, r0, Ep(i), 1, R, Ap(i), 1, R, false, sc);
+          }
       }
       k[0] = k0n;
       // ================= modes n >= 1 (stitch_nontemporal_unfolding, stitch.cpp:75-108)
@@ -751,7 +744,7 @@ __global__ void __launch_bounds__(kStitchThreads, kStitchCtas)
             double* dst = TB[step & 1] + int64_t(i) * lay.chain;
             if (m == 0) {
               const double* A0 = parts[i].partial ? Ap(i) : Ep(i);
-              return bg_mode_product(parts[i].core, 1, cur[0], prod_range(cur, 1, p), A0, cur[0], 1, k[0], dst);
+              return bg_mode_product(parts[i].core, 1, cur[0], prod_range(cur, 1, p), A0, R, 1, k[0], dst);
             }
             const double* src = TB[(step - 1) & 1] + int64_t(i) * lay.chain;
             return bg_mode_product(src, prod_range(cur, 0, m), cur[m], prod_range(cur, m + 1, p), Pm(i, m), 1, k[m],
@@ -804,7 +797,16 @@ __global__ void __launch_bounds__(kStitchThreads, kStitchCtas)
             for (int i = 0; i < s; ++i) {
               const double* V = vptr[i] + a;
               const int64_t j0 = foff[i], rn = foff[i + 1] - j0;
-              for (int64_t j = 0; j < rn; ++j) {
+              int64_t j = 0;
+              for (; j + 3 < rn; j += 4) {  // four V loads in flight
+                const double v0 = V[j * dn], v1 = V[(j + 1) * dn], v2 = V[(j + 2) * dn], v3 = V[(j + 3) * dn];
+                const double* fr = Fs + (j0 + j) * Qn + c0;
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                  if (c0 + c < Qn)
+                    acc[c] = fma(v3, fr[c + 3 * Qn], fma(v2, fr[c + 2 * Qn], fma(v1, fr[c + Qn], fma(v0, fr[c], acc[c]))));
+              }
+              for (; j < rn; ++j) {
                 const double v = V[j * dn];
                 const double* fr = Fs + (j0 + j) * Qn + c0;
 #pragma unroll
@@ -847,7 +849,7 @@ __global__ void __launch_bounds__(kStitchThreads, kStitchCtas)
     double* U0 = D.out_f[0];
     const long long tu = tstart();
     if (any_zero_sigma ||
-        !materialize_u0(int(k0), parts, s, ws + lay.E, lay.per_part_E, U0, D.L, flips, idxbuf, dsm, sc)) {
+        !materialize_u0(int(k0), parts, s, Est, R, roff, U0, D.L, flips, idxbuf, dsm, sc)) {
       // Row-parallel materialisation in column chunks of KU: each thread owns
       // rows, keeps the first max-|.| row per column (sign convention), then a
       // block argmax picks each column's sign. Rows of part i: Vsub_i[r,:] E_i.
@@ -867,7 +869,7 @@ __global__ void __launch_bounds__(kStitchThreads, kStitchCtas)
           const PartView pv = load_part(parts[i]);
           const int64_t r0 = pv.rho[0];
           const double* vs = pv.v0 + pv.row0;
-          const double* E = Ep(i) + c0 * r0;
+          const double* E = Ep(i) + c0 * R;
           for (int64_t r = threadIdx.x; r < pv.len; r += blockDim.x) {
             double out[KU];
   #pragma unroll
@@ -876,7 +878,7 @@ __global__ void __launch_bounds__(kStitchThreads, kStitchCtas)
               const double v = vs[r + a * pv.ld0];
   #pragma unroll
               for (int c = 0; c < KU; ++c)
-                if (c < nc) out[c] = fma(v, E[a + c * r0], out[c]);
+                if (c < nc) out[c] = fma(v, E[a + c * R], out[c]);
             }
   #pragma unroll
             for (int c = 0; c < KU; ++c)
