@@ -515,9 +515,103 @@ static __device__ bool llsv_subspace(const double* P, int64_t outer, int64_t row
   return it > 0;
 }
 
+// Top-k eigenvectors of a symmetric positive semidefinite n x n matrix G
+// (col-major, ld n) by warm-started block subspace iteration: W = G U,
+// B = U^T W, stop when ||W - U B||_F <= 1e-13 ||B||_F, else U = orth(W)
+// (CholeskyQR2); a Rayleigh-Ritz rotation by the eigenvectors of B then gives
+// the eigenvectors in descending order (the same vectors a full Jacobi solve
+// returns, to rounding). U holds the start on entry (n x K, any basis of full
+// rank); W is scratch of the same size. Returns the buffer holding the result
+// (U or W) and the eigenvalues in lam[0..K), or nullptr on breakdown or no
+// convergence (rank-deficient G, tiny gap) — the caller then runs Jacobi.
+// Replaces an O(n^3)-per-sweep Jacobi solve of the whole Gram matrix when only
+// k << n vectors are needed (Gram sizes 64..100 at BASELINE configs C3/C4).
+template <int K>
+__device__ __noinline__ double* sym_topk_si_k(const double* __restrict__ G, int n, double* U, double* W,
+                                              double* lam, int* order, double* dsm, BlockScratch& sc) {
+  double* small = dsm + 768;  // CholeskyQR scratch (3 K^2); dsm[0, 768) is the Rayleigh-Ritz eigensolver's
+  double* B = dsm + 1536;     // K x K
+  if (!cholqr_pass_k<K>(U, n, small, sc) || !cholqr_pass_k<K>(U, n, small, sc)) return nullptr;
+  bool conv = false;
+  int it = 0;
+  for (; it < kSiMaxIter; ++it) {
+    for (int idx = threadIdx.x; idx < n * K; idx += blockDim.x) {
+      const int i = idx % n, j = idx / n;
+      W[idx] = dot4(G + int64_t(i) * n, 1, U + int64_t(j) * n, 1, n);
+    }
+    __syncthreads();
+    gemm(K, K, n, U, n, 1, W, 1, n, B, 1, K, false, sc);  // B = U^T W
+    double rsq = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      double u[K];
+#pragma unroll
+      for (int l = 0; l < K; ++l) u[l] = U[i + l * n];
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        double v = W[i + j * n];
+#pragma unroll
+        for (int l = 0; l < K; ++l) v = fma(-u[l], B[l + j * K], v);
+        rsq = fma(v, v, rsq);
+      }
+    }
+    double bsq = 0.0;
+    for (int e = threadIdx.x; e < K * K; e += blockDim.x) bsq = fma(B[e], B[e], bsq);
+    rsq = block_sum(rsq, sc);
+    bsq = block_sum(bsq, sc);
+    if (!(bsq > 0.0)) return nullptr;
+    if (rsq <= 1e-26 * bsq) {
+      conv = true;
+      break;
+    }
+    double* t = U;  // U <- orth(W)
+    U = W;
+    W = t;
+    if (!cholqr_pass_k<K>(U, n, small, sc) || !cholqr_pass_k<K>(U, n, small, sc)) return nullptr;
+  }
+  if (!conv) return nullptr;
+  if (threadIdx.x == 0) sc.si_iters += it + 1;
+  double* diag = nullptr;
+  const double* R = eig_run(B, K, small, order, dsm, &diag, sc);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double u[K];
+#pragma unroll
+    for (int l = 0; l < K; ++l) u[l] = U[i + l * n];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const double* rj = R + order[j] * K;
+      double v = 0.0;
+#pragma unroll
+      for (int l = 0; l < K; ++l) v = fma(u[l], rj[l], v);
+      W[i + j * n] = v;
+    }
+  }
+  if (threadIdx.x < K) lam[threadIdx.x] = diag[order[threadIdx.x] * (K + 1)];
+  __syncthreads();
+  return W;
+}
+
+static __device__ double* sym_topk_si(const double* G, int n, int k, double* U, double* W, double* lam, int* order,
+                                      double* dsm, BlockScratch& sc) {
+  switch (k) {
+#define TT_CASE(N) \
+  case N:          \
+    return sym_topk_si_k<N>(G, n, U, W, lam, order, dsm, sc);
+    TT_CASE(1) TT_CASE(2) TT_CASE(3) TT_CASE(4) TT_CASE(5) TT_CASE(6) TT_CASE(7) TT_CASE(8)
+    TT_CASE(9) TT_CASE(10) TT_CASE(11) TT_CASE(12) TT_CASE(13) TT_CASE(14) TT_CASE(15) TT_CASE(16)
+#undef TT_CASE
+    default:
+      return nullptr;
+  }
+}
+
+// Gram sizes above this use the warm-started top-k subspace iteration instead
+// of a full Jacobi solve (when the caller has a warm start).
+constexpr int kGramSiMinN = 24;
+
 // leading_left_singular_vectors (linalg.cpp:45-64) of the mode unfolding of a
 // row-major (outer, rows, inner) tensor, through the Gram matrix of its
-// smaller side. U: rows x k (ld rows), sign-fixed.
+// smaller side. U: rows x k (ld rows), sign-fixed. On entry U holds the
+// factor's current value (kprev columns), used as the iterations' warm start.
 static __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows, int64_t inner, int64_t k, double* U,
                             double* G, double* V, double* misc, double* dsm, BlockScratch& sc, int64_t kprev = 0,
                             double* si = nullptr) {
@@ -535,30 +629,64 @@ static __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows,
   }
   int* order = reinterpret_cast<int*>(misc);
   double* sig = misc + kMisc / 2;
-  double* diag = nullptr;
-  if (rows <= cols) {
-    const int n = int(rows);
-    long long tg = tstart();
+  double* lamv = misc + kMisc / 2 + 512;
+  const bool wide = rows <= cols;
+  const int n = int(wide ? rows : cols);
+  long long tg = tstart();
+  if (wide) {
     if (inner == 1)  // A = P^T viewed (rows x outer): a GEMM with the K split across the block
       gemm(rows, rows, outer, P, 1, rows, P, rows, 1, G, 1, rows, false, sc);
     else
       gram_rows(P, outer, rows, inner, G);
-    tstop(sc, kPhGram, tg);
-    const double* Vp = eig_run(G, n, V, order, dsm, &diag, sc);
+  } else {
+    gram_cols(P, outer, rows, inner, G);
+  }
+  tstop(sc, kPhGram, tg);
+  // eigenvectors: column c at vcol(c), eigenvalue lamc(c), descending
+  const double* Vsi = nullptr;
+  if (kprev > 0 && k <= kSiMaxK && n > kGramSiMinN && n >= 2 * k && 1792 <= sc.dsm_cap) {
+    const long long t0 = tstart();
+    double* Us = V;
+    double* Ws = V + int64_t(n) * k;
+    const int64_t kp = imin(kprev, k);
+    for (int64_t idx = threadIdx.x; idx < n * k; idx += blockDim.x) {
+      const int64_t r = idx % n, c = idx / n;
+      double v;
+      if (c >= kp) {
+        v = (r == (c * 7919) % n) ? 1.0 : 0.0;  // pad with canonical vectors
+      } else if (wide) {
+        v = U[r + c * rows];
+      } else {  // tall: A^T U_prev, column r of the unfolding
+        const int64_t o = r / inner, t = r - o * inner;
+        v = dot4(P + o * rows * inner + t, inner, U + c * rows, 1, rows);
+      }
+      Us[idx] = v;
+    }
+    __syncthreads();
+    Vsi = sym_topk_si(G, n, int(k), Us, Ws, lamv, order, dsm, sc);
+    tstop(sc, kPhEig, t0);
+    if (threadIdx.x == 0) {
+      if (Vsi)
+        sc.si_ok += 1;
+      else
+        sc.si_fail += 1;
+    }
+  }
+  double* diag = nullptr;
+  const double* Vp = Vsi;
+  if (!Vsi) Vp = eig_run(G, n, V, order, dsm, &diag, sc);
+  auto vcol = [&](int64_t c) { return Vsi ? Vsi + c * n : Vp + int64_t(order[c]) * n; };
+  auto lamc = [&](int64_t c) { return Vsi ? lamv[c] : diag[order[c] * (n + 1)]; };
+  if (wide) {
     for (int64_t idx = threadIdx.x; idx < rows * k; idx += blockDim.x) {
       const int64_t i = idx % rows, c = idx / rows;
-      U[idx] = Vp[i + int64_t(order[c]) * n];
+      U[idx] = vcol(c)[i];
     }
     __syncthreads();
   } else {
-    const int n = int(cols);
-    long long tg = tstart();
-    gram_cols(P, outer, rows, inner, G);
-    tstop(sc, kPhGram, tg);
-    const double* Vp = eig_run(G, n, V, order, dsm, &diag, sc);
     if (threadIdx.x < k) {
-      const double l0 = fmax(diag[order[0] * (n + 1)], 0.0);
-      const double lc = fmax(diag[order[threadIdx.x] * (n + 1)], 0.0);
+      const double l0 = fmax(lamc(0), 0.0);
+      const double lc = fmax(lamc(threadIdx.x), 0.0);
       sig[threadIdx.x] = gram_sigma_ok(lc, l0) ? 1.0 / sqrt(lc) : 0.0;
     }
     __syncthreads();
@@ -568,12 +696,8 @@ static __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows,
       const double inv = sig[c];
       double s = 0.0;
       if (inv != 0.0) {
-        const double* vc = Vp + int64_t(order[c]) * n;
-        for (int64_t o = 0; o < outer; ++o) {
-          const double* a = P + (o * rows + i) * inner;
-          const double* v = vc + o * inner;
-          for (int64_t t = 0; t < inner; ++t) s = fma(a[t], v[t], s);
-        }
+        const double* vc = vcol(c);
+        for (int64_t o = 0; o < outer; ++o) s += dot4(P + (o * rows + i) * inner, 1, vc + o * inner, 1, inner);
       }
       U[idx] = s * inv;
     }

@@ -404,15 +404,17 @@ __global__ void __launch_bounds__(kStitchThreads, kStitchCtas)
       // a fixed number of block passes whatever s is.
       bool mode0_done = false;
       const int kk = int(k0n);
-      constexpr int kSiE = 2560;  // shared-memory offset of E (below: eig scratch, Y, small matrices)
-      if (kk <= kSiMaxK && Q >= 2 * kk && Q * kk <= kSiMaxYK && R >= kk && kSiE + 2 * R * kk <= sc.dsm_cap) {
+      // shared memory: [0, 768) Rayleigh-Ritz eigensolver scratch, Y (Q x k),
+      // G/L/Linv/B (k x k), E and A (R x k each)
+      const int64_t si_smem = 768 + Q * kk + 5 * kk * kk + 2 * int64_t(R) * kk;
+      if (kk <= kSiMaxK && Q >= 2 * kk && R >= kk && si_smem <= sc.dsm_cap) {
         const long long t_si = tstart();
         const int nt = int(blockDim.x);
         const int Qi = int(Q);
         double* Y = dsm + 768;            // Q x kk
-        double* small = dsm + 1280;       // G, L, Linv (kk x kk each)
+        double* small = Y + Q * kk;       // G, L, Linv (kk x kk each)
         double* B = small + 4 * kk * kk;  // kk x kk
-        double* Es = dsm + kSiE;          // R x kk (ld R)
+        double* Es = B + kk * kk;         // R x kk (ld R)
         double* As = Es + R * kk;         // R x kk (ld R)
         double* Rg = Z;                   // residual rows of partial parts (ld R)
         // dst = S src (entire rows: S = I); both stacked, ld R

@@ -67,6 +67,9 @@ def assert_factors_match(x, got, want, where="", check_angles=True, gap_tol=1e-6
     ((30, 10, 5), (3, 3, 3), 8),
     ((1, 8, 8), (3, 3, 3), 9),
     ((10, 4, 3, 2, 3), (2, 2, 2, 2, 2), 10),
+    # Gram sizes 64..100: warm-started top-k subspace iteration on the Gram matrix (C3 / C4 leaf shapes)
+    ((64, 500, 88), (10, 10, 10), 11),
+    ((64, 64, 64, 8), (8, 8, 8, 4), 12),
 ])
 def test_tucker_als_matches_oracle(E, shape, ranks, seed):
     rng = np.random.default_rng(seed)
@@ -238,6 +241,19 @@ def test_tree_matrix_series_and_5way(E):
 def test_tree_4way_config4_like(E):
     series = _series((256, 16, 16, 8), (8, 8, 8, 4), 0.05, 4)
     _compare_trees(E, series, (8, 8, 8, 4), 32, queries=_ranges(256, 20, 4))
+
+
+def test_tree_config3_like(E):
+    # C3 dims at reduced T: (T=320, 500, 88), ranks (10, 10, 10), leaf 64 (4 leaves + a raw tail);
+    # Gram sizes 88..100 take the top-k subspace-iteration path
+    series = _series((320, 500, 88), (10, 10, 10), 0.3, 3)
+    _compare_trees(E, series, (10, 10, 10), 64, queries=_ranges(320, 12, 3, minlen=2))
+
+
+def test_tree_config4_dims(E):
+    # C4 dims at reduced T: (T=256, 64, 64, 8), ranks (8, 8, 8, 4), leaf 64; 64 x 256 unfoldings
+    series = _series((256, 64, 64, 8), (8, 8, 8, 4), 0.05, 4)
+    _compare_trees(E, series, (8, 8, 8, 4), 64, queries=_ranges(256, 16, 4))
 
 
 def test_query_short_ranges_rank_shrink(E):
