@@ -315,6 +315,83 @@ __device__ __forceinline__ void gram_rows(const double* __restrict__ P, int64_t 
   __syncthreads();
 }
 
+// Register-tiled Gram for larger n: G (n x n, col-major) = sum_x T(x, :)^T T(x, :)
+// with T(x, a) = elem(x, a), x < nx. Chunks of x are staged in shared memory
+// (cx x n, row-major; `x_fast` picks the staging order so that consecutive
+// threads read consecutive global addresses), and each thread accumulates a
+// 4x4 block of the upper triangle in registers: per staged row, 8 shared loads
+// feed 16 FMAs, against 2 uncoalesced global loads per FMA for a
+// thread-per-entry Gram. Blocks beyond one per thread take further passes.
+template <class Elem>
+__device__ __forceinline__ void gram_tiled(int n, int64_t nx, Elem elem, bool x_fast, double* __restrict__ G,
+                                           double* stage, int stage_cap) {
+  const int nb = (n + 3) / 4;
+  const int ntiles = nb * (nb + 1) / 2;
+  const int ch = int(imax(1, imin(nx, stage_cap / n)));
+  for (int tile0 = 0; tile0 < ntiles; tile0 += blockDim.x) {
+    const int tile = tile0 + threadIdx.x;
+    int bi = 0, bj = 0;
+    if (tile < ntiles) {  // tile -> (bi <= bj), row-major over the upper triangle
+      int e = tile;
+      while (e >= nb - bi) {
+        e -= nb - bi;
+        ++bi;
+      }
+      bj = bi + e;
+    }
+    double acc[4][4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[p][q] = 0.0;
+    for (int64_t x0 = 0; x0 < nx; x0 += ch) {
+      const int cx = int(imin(ch, nx - x0));
+      __syncthreads();
+      if (x_fast) {
+        for (int idx = threadIdx.x; idx < cx * n; idx += blockDim.x) {
+          const int x = idx % cx, a = idx / cx;
+          stage[x * n + a] = elem(x0 + x, a);
+        }
+      } else {
+        for (int idx = threadIdx.x; idx < cx * n; idx += blockDim.x) {
+          const int a = idx % n, x = idx / n;
+          stage[x * n + a] = elem(x0 + x, a);
+        }
+      }
+      __syncthreads();
+      if (tile < ntiles) {
+        const int i0 = 4 * bi, j0 = 4 * bj;
+        for (int x = 0; x < cx; ++x) {
+          const double* row = stage + x * n;
+          double u[4], v[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            u[q] = i0 + q < n ? row[i0 + q] : 0.0;
+            v[q] = j0 + q < n ? row[j0 + q] : 0.0;
+          }
+#pragma unroll
+          for (int p = 0; p < 4; ++p)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[p][q] = fma(u[p], v[q], acc[p][q]);
+        }
+      }
+    }
+    if (tile < ntiles) {
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = 4 * bi + p, j = 4 * bj + q;
+          if (i < n && j < n && i <= j) {
+            G[i + int64_t(j) * n] = acc[p][q];
+            G[j + int64_t(i) * n] = acc[p][q];
+          }
+        }
+    }
+  }
+  __syncthreads();
+}
+
 // G = A^T A (cols x cols), cols = outer*inner.
 __device__ __forceinline__ void gram_cols(const double* __restrict__ P, int64_t outer, int64_t rows, int64_t inner,
                                           double* __restrict__ G) {

@@ -607,6 +607,8 @@ static __device__ double* sym_topk_si(const double* G, int n, int k, double* U, 
 // Gram sizes above this use the warm-started top-k subspace iteration instead
 // of a full Jacobi solve (when the caller has a warm start).
 constexpr int kGramSiMinN = 24;
+// Gram sizes from this up use the register-tiled Gram.
+constexpr int kGramTiledMinN = 24;
 
 // leading_left_singular_vectors (linalg.cpp:45-64) of the mode unfolding of a
 // row-major (outer, rows, inner) tensor, through the Gram matrix of its
@@ -633,7 +635,17 @@ static __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows,
   const bool wide = rows <= cols;
   const int n = int(wide ? rows : cols);
   long long tg = tstart();
-  if (wide) {
+  // unfolding element A(i, c) = P[(o*rows + i)*inner + t], c = o*inner + t
+  auto unf = [&](int64_t i, int64_t c) {
+    const int64_t o = c / inner, t = c - o * inner;
+    return P[(o * rows + i) * inner + t];
+  };
+  if (n >= kGramTiledMinN && n * 4 <= sc.dsm_cap) {
+    if (wide)  // G = A A^T: x runs over the columns c (contiguous in t)
+      gram_tiled(n, cols, [&](int64_t c, int a) { return unf(a, c); }, true, G, dsm, sc.dsm_cap);
+    else  // G = A^T A: x runs over the rows i, a over the columns
+      gram_tiled(n, rows, [&](int64_t i, int a) { return unf(i, a); }, false, G, dsm, sc.dsm_cap);
+  } else if (wide) {
     if (inner == 1)  // A = P^T viewed (rows x outer): a GEMM with the K split across the block
       gemm(rows, rows, outer, P, 1, rows, P, rows, 1, G, 1, rows, false, sc);
     else
