@@ -161,6 +161,31 @@ tt_status tt_last_redecomposed(const tt_tree* tree, int64_t* ids, int64_t cap, i
  * them newline-separated into buf.                         sst.hpp:74-78 */
 int32_t tt_validate(const tt_tree* tree, char* buf, int64_t cap);
 
+/* ---- persistence (io.hpp:11-31) ------------------------------------------- */
+/* write_tree_file(path, tree): the reference's "SST1" container, bit-exact in
+ * layout (header, config, node table, per-node core + row-major factors).
+ * A tree with leaf_block B > 1 or a raw tail appends a "TTB1" extension after
+ * the node table (u64 B | u64 tail slices | row-major f64 tail), which the
+ * reference reader ignores. Node payloads are downloaded from the device.
+ * Errors: TT_EIO (std::runtime_error in io.cpp:19).           io.cpp:165-188 */
+tt_status tt_tree_save(const tt_tree* tree, const char* path);
+
+/* read_tree_file(path): rebuilds a tree on `device` from an SST1 file (node
+ * payloads uploaded into the device slots). flags: TT_FLAG_STRUCTURE_ONLY
+ * loads the bookkeeping only (no device).                     io.cpp:190-230 */
+tt_status tt_tree_load(const char* path, int32_t device, int32_t flags, tt_tree** out);
+
+/* StreamSegmentTree::config() (sst.hpp:66): the tree's configuration.      */
+tt_status tt_tree_config(const tt_tree* tree, tt_config* out);
+
+/* "TTS1" tensor container (io.hpp:11-19): magic | u16 version=1 | u8 p |
+ * p x u64 dims | row-major f64 payload. Host memory only.     io.cpp:124-150 */
+tt_status tt_tensor_write(const char* path, int32_t p, const int64_t* dims, const double* data);
+/* Reads the header (p, dims[0..p), dims holding TT_TENSOR_MAX_ORDER entries);
+ * with data != NULL also the payload (prod(dims) doubles).                  */
+#define TT_TENSOR_MAX_ORDER 32
+tt_status tt_tensor_read(const char* path, int32_t* p, int64_t* dims, double* data);
+
 /* ---- queries (query.hpp:33-50) -------------------------------------------- */
 /* recall(tree, ts, te, theta); theta = NaN selects the tree's theta
  * (std::nullopt in the reference).                                          */

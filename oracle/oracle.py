@@ -71,6 +71,8 @@ def lib():
             "orc_tree_query_batch": (C.c_int, [vp, i64ptr, i64, C.c_double, C.c_int, dptr]),
             "orc_tree_validate": (C.c_int, [vp, C.c_char_p, i64]),
             "orc_tree_tail": (dptr, [vp]),
+            "orc_tree_save": (C.c_int, [vp, C.c_char_p]),
+            "orc_tensor_write": (C.c_int, [C.c_char_p, C.c_int, i64ptr, dptr]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -274,6 +276,15 @@ def generate_synthetic(shape, true_ranks, noise=0.0, seed=20240117) -> np.ndarra
     return out.reshape(shape)
 
 
+def write_tensor(path: str, x: np.ndarray):
+    """write_tensor_file restated (io.cpp:124-133)."""
+    a = np.ascontiguousarray(x, dtype=np.float64)
+    d, dp = _i(list(a.shape))
+    code = lib().orc_tensor_write(os.fsencode(path), a.ndim, dp, _d(a))
+    if code:
+        _raise(code)
+
+
 def reconstruct(f: Factors) -> np.ndarray:
     L = lib()
     h = _make(f)
@@ -345,6 +356,12 @@ class Tree:
         if s.size % ss:
             raise InvalidArgument("append: slice shape does not match tree")
         code = lib().orc_tree_append(self._h, _d(s), s.size // ss)
+        if code:
+            _raise(code)
+
+    def save(self, path: str):
+        """write_tree_file restated (io.cpp:165-188; + TTB1 extension for B > 1)."""
+        code = lib().orc_tree_save(self._h, os.fsencode(path))
         if code:
             _raise(code)
 

@@ -1,6 +1,9 @@
 // TEST INFRASTRUCTURE ONLY — flat C API over the oracle for the Python tests
 // (tests/, oracle/oracle.py) and the CPU baseline arm of bench.py.
+#include <algorithm>
 #include <atomic>
+#include <cstdio>
+#include <stdexcept>
 #include <chrono>
 #include <cstring>
 #include <exception>
@@ -36,6 +39,25 @@ struct orc_factors {
 struct orc_tree {
   Tree t;
 };
+
+namespace {
+struct OWriter {
+  std::FILE* f;
+  explicit OWriter(const char* p) : f(std::fopen(p, "wb")) {
+    if (!f) throw std::runtime_error(std::string("cannot open ") + p + " for writing");
+  }
+  ~OWriter() {
+    if (f) std::fclose(f);
+  }
+  void bytes(const void* b, std::size_t n) {
+    if (n && std::fwrite(b, 1, n, f) != n) throw std::runtime_error("write failed");
+  }
+  template <class T>
+  void le(T v) {
+    bytes(&v, sizeof(T));
+  }
+};
+}  // namespace
 
 extern "C" {
 
@@ -357,5 +379,81 @@ int orc_tree_validate(const orc_tree* t, char* buf, std::int64_t cap) {
 
 // Raw tail slices (row-major), count = timespan - leaves*B.
 const double* orc_tree_tail(const orc_tree* t) { return t->t.tail().v.data(); }
+
+
+// ---- persistence: restatement of write_tree / write_tensor (io.cpp:87-101,
+// 124-133, 165-188), little-endian field by field; trees with a leaf block
+// B > 1 or a raw tail append the engine's "TTB1" extension (u16 version,
+// u64 B, u64 tail slices, row-major tail) after the node table.
+
+int orc_tree_save(const orc_tree* h, const char* path) {
+  try {
+    const Tree& t = h->t;
+    const TreeConfig& cfg = t.config();
+    OWriter w(path);
+    w.bytes("SST1", 4);
+    w.le<std::uint16_t>(1);
+    w.le<std::uint64_t>(static_cast<std::uint64_t>(t.timespan()));
+    w.le<std::uint8_t>(static_cast<std::uint8_t>(cfg.nontemporal.size() + 1));
+    for (Index d : cfg.nontemporal) w.le<std::uint64_t>(static_cast<std::uint64_t>(d));
+    for (Index r : cfg.ranks) w.le<std::uint64_t>(static_cast<std::uint64_t>(r));
+    w.le<double>(cfg.theta);
+    w.le<std::uint32_t>(static_cast<std::uint32_t>(cfg.als.max_iters));
+    w.le<double>(cfg.als.tol);
+    w.le<std::uint64_t>(cfg.als.seed);
+    w.le<std::uint64_t>(static_cast<std::uint64_t>(t.stitch_count()));
+    w.le<std::uint64_t>(static_cast<std::uint64_t>(t.root()));
+    w.le<std::uint64_t>(static_cast<std::uint64_t>(t.nodes().size()));
+    for (const Node& v : t.nodes()) {
+      w.le<std::uint64_t>(static_cast<std::uint64_t>(v.id));
+      w.le<std::uint64_t>(static_cast<std::uint64_t>(v.begin));
+      w.le<std::uint64_t>(static_cast<std::uint64_t>(v.end));
+      w.le<std::uint8_t>(static_cast<std::uint8_t>(v.kind));
+      w.le<std::uint64_t>(static_cast<std::uint64_t>(v.left));
+      w.le<std::uint64_t>(static_cast<std::uint64_t>(v.right));
+      w.le<std::uint8_t>(v.dec ? 1 : 0);
+      if (!v.dec) continue;
+      const Factors& f = *v.dec;
+      w.le<std::uint8_t>(static_cast<std::uint8_t>(f.order()));
+      for (Index n = 0; n < f.order(); ++n) w.le<std::uint64_t>(static_cast<std::uint64_t>(f.core.dim(n)));
+      w.bytes(f.core.v.data(), f.core.v.size() * sizeof(double));
+      for (const Mat& u : f.f) {
+        w.le<std::uint64_t>(static_cast<std::uint64_t>(u.rows));
+        w.le<std::uint64_t>(static_cast<std::uint64_t>(u.cols));
+        for (Index i = 0; i < u.rows; ++i)
+          for (Index j = 0; j < u.cols; ++j) w.le<double>(u(i, j));
+      }
+    }
+    const Index tail = t.timespan() - t.leaves() * cfg.leaf_block;
+    if (cfg.leaf_block > 1 || tail > 0) {
+      w.bytes("TTB1", 4);
+      w.le<std::uint16_t>(1);
+      w.le<std::uint64_t>(static_cast<std::uint64_t>(cfg.leaf_block));
+      w.le<std::uint64_t>(static_cast<std::uint64_t>(tail));
+      w.bytes(t.tail().v.data(), t.tail().v.size() * sizeof(double));  // exactly `tail` slices
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int orc_tensor_write(const char* path, int p, const std::int64_t* dims, const double* data) {
+  try {
+    OWriter w(path);
+    w.bytes("TTS1", 4);
+    w.le<std::uint16_t>(1);
+    w.le<std::uint8_t>(static_cast<std::uint8_t>(p));
+    std::size_t n = 1;
+    for (int m = 0; m < p; ++m) {
+      w.le<std::uint64_t>(static_cast<std::uint64_t>(dims[m]));
+      n *= static_cast<std::size_t>(dims[m]);
+    }
+    w.bytes(data, n * sizeof(double));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
 
 }  // extern "C"

@@ -1766,3 +1766,340 @@ const double* tt_factors_objective(const tt_factors* f) { return f ? f->objectiv
 void tt_factors_free(tt_factors* f) { delete f; }
 
 }  // extern "C"
+
+// ===========================================================================
+// Persistence: the reference's SST1 / TTS1 containers (io.hpp:11-31,
+// io.cpp:87-239), little-endian, written field by field in the reference's
+// order. Host-side I/O only; node payloads move through the device slots.
+namespace {
+
+constexpr char kTreeMagic[4] = {'S', 'S', 'T', '1'};
+constexpr char kTensorMagic[4] = {'T', 'T', 'S', '1'};
+constexpr char kBlockMagic[4] = {'T', 'T', 'B', '1'};  // engine extension: leaf block + raw tail
+constexpr uint16_t kFormatVersion = 1;
+
+struct Writer {
+  std::FILE* f;
+  std::string path;
+  explicit Writer(const char* p) : f(std::fopen(p, "wb")), path(p) {
+    if (!f) fail(TT_EIO, std::string("cannot open ") + p + " for writing");
+  }
+  ~Writer() {
+    if (f) std::fclose(f);
+  }
+  void bytes(const void* b, size_t n) {
+    if (n && std::fwrite(b, 1, n, f) != n) fail(TT_EIO, "failed writing " + path);
+  }
+  template <class T>
+  void le(T v) {  // x86-64 is little-endian: the in-memory bytes are the file bytes
+    bytes(&v, sizeof(T));
+  }
+  void close() {
+    if (std::fclose(f) != 0) {
+      f = nullptr;
+      fail(TT_EIO, "failed writing " + path);
+    }
+    f = nullptr;
+  }
+};
+
+struct Reader {
+  std::FILE* f;
+  explicit Reader(const char* p) : f(std::fopen(p, "rb")) {
+    if (!f) fail(TT_EIO, std::string("cannot open ") + p);
+  }
+  ~Reader() {
+    if (f) std::fclose(f);
+  }
+  bool try_bytes(void* b, size_t n) { return std::fread(b, 1, n, f) == n; }
+  void bytes(void* b, size_t n, const char* what) {  // io.cpp:40-47
+    if (n && !try_bytes(b, n)) fail(TT_EIO, std::string("truncated input reading ") + what);
+  }
+  template <class T>
+  T le(const char* what) {
+    T v;
+    bytes(&v, sizeof(T), what);
+    return v;
+  }
+  Index extent(const char* what) {  // io.cpp:62-70
+    const uint64_t v = le<uint64_t>(what);
+    if (v > uint64_t(1) << 40) fail(TT_EIO, std::string("implausible extent in ") + what);
+    return static_cast<Index>(v);
+  }
+  void magic(const char* m, const char* what) {  // io.cpp:76-85
+    char got[4];
+    bytes(got, 4, what);
+    if (std::memcmp(got, m, 4) != 0) fail(TT_EIO, std::string("bad magic for ") + what);
+    const uint16_t version = le<uint16_t>(what);
+    if (version != kFormatVersion)
+      fail(TT_EIO, "unsupported version " + std::to_string(version) + " for " + what);
+  }
+};
+
+// write_factors (io.cpp:87-101): u8 p | core dims | core | per mode rows, cols, row-major entries
+void write_node_factors(Writer& w, const tt_tree& t, const HostNode& v) {
+  const int p = t.p;
+  w.le<uint8_t>(static_cast<uint8_t>(p));
+  for (int m = 0; m < p; ++m) w.le<uint64_t>(static_cast<uint64_t>(v.ranks[m]));
+  std::vector<double> core(static_cast<size_t>(prod_range(v.ranks, 0, p)));
+  std::vector<std::vector<double>> f(static_cast<size_t>(p));
+  std::vector<double*> fp(static_cast<size_t>(p));
+  for (int m = 0; m < p; ++m) {
+    const Index rows = m == 0 ? v.length() : t.d[m];
+    f[m].resize(static_cast<size_t>(rows * v.ranks[m]));
+    fp[m] = f[m].data();
+  }
+  DeviceGuard g(t.ex->device);
+  cuda_check(cudaMemcpyAsync(core.data(), v.core, core.size() * sizeof(double), cudaMemcpyDeviceToHost, t.ex->stream),
+             "node core download");
+  for (int m = 0; m < p; ++m)
+    cuda_check(cudaMemcpyAsync(fp[m], v.f[m], f[m].size() * sizeof(double), cudaMemcpyDeviceToHost, t.ex->stream),
+               "node factor download");
+  t.ex->sync();
+  w.bytes(core.data(), core.size() * sizeof(double));
+  std::vector<double> rowmajor;
+  for (int m = 0; m < p; ++m) {
+    const Index rows = m == 0 ? v.length() : t.d[m], cols = v.ranks[m];
+    w.le<uint64_t>(static_cast<uint64_t>(rows));
+    w.le<uint64_t>(static_cast<uint64_t>(cols));
+    rowmajor.resize(static_cast<size_t>(rows * cols));
+    for (Index i = 0; i < rows; ++i)
+      for (Index j = 0; j < cols; ++j) rowmajor[size_t(i * cols + j)] = f[m][size_t(i + j * rows)];
+    w.bytes(rowmajor.data(), rowmajor.size() * sizeof(double));
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+tt_status tt_tree_save(const tt_tree* t, const char* path) {
+  return guarded([&] {
+    if (!t || !path) fail(TT_EINVAL, "tt_tree_save: null argument");
+    if (t->structure_only) fail(TT_ELOGIC, "tt_tree_save: a structure-only tree has no payloads");
+    std::lock_guard<std::mutex> lk(t->qmu);
+    Writer w(path);
+    // write_tree (io.cpp:165-188)
+    w.bytes(kTreeMagic, 4);
+    w.le<uint16_t>(kFormatVersion);
+    w.le<uint64_t>(static_cast<uint64_t>(t->timespan));
+    w.le<uint8_t>(static_cast<uint8_t>(t->p));
+    for (int m = 1; m < t->p; ++m) w.le<uint64_t>(static_cast<uint64_t>(t->d[m]));
+    for (int m = 0; m < t->p; ++m) w.le<uint64_t>(static_cast<uint64_t>(t->cfg.ranks[m]));
+    w.le<double>(t->cfg.theta);
+    w.le<uint32_t>(static_cast<uint32_t>(t->cfg.max_iters));
+    w.le<double>(t->cfg.tol);
+    w.le<uint64_t>(t->cfg.seed);
+    w.le<uint64_t>(static_cast<uint64_t>(t->stitch_count));
+    w.le<uint64_t>(static_cast<uint64_t>(t->root));
+    w.le<uint64_t>(static_cast<uint64_t>(t->nodes.size()));
+    for (const HostNode& v : t->nodes) {
+      w.le<uint64_t>(static_cast<uint64_t>(v.id));
+      w.le<uint64_t>(static_cast<uint64_t>(v.begin));
+      w.le<uint64_t>(static_cast<uint64_t>(v.end));
+      w.le<uint8_t>(static_cast<uint8_t>(v.kind));
+      w.le<uint64_t>(static_cast<uint64_t>(v.left));
+      w.le<uint64_t>(static_cast<uint64_t>(v.right));
+      w.le<uint8_t>(v.has_dec ? 1 : 0);
+      if (v.has_dec) write_node_factors(w, *t, v);
+    }
+    const Index tail = t->timespan - t->leaves * t->B;
+    if (t->B > 1 || tail > 0) {  // engine extension (ignored by the reference reader)
+      w.bytes(kBlockMagic, 4);
+      w.le<uint16_t>(kFormatVersion);
+      w.le<uint64_t>(static_cast<uint64_t>(t->B));
+      w.le<uint64_t>(static_cast<uint64_t>(tail));
+      std::vector<double> buf(static_cast<size_t>(tail * t->slice));
+      if (!buf.empty()) {
+        DeviceGuard g(t->ex->device);
+        cuda_check(cudaMemcpyAsync(buf.data(), t->tail.p, buf.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                                   t->ex->stream),
+                   "tail download");
+        t->ex->sync();
+      }
+      w.bytes(buf.data(), buf.size() * sizeof(double));
+    }
+    w.close();
+  });
+}
+
+tt_status tt_tree_load(const char* path, int32_t device, int32_t flags, tt_tree** out) {
+  return guarded([&] {
+    if (!path || !out) fail(TT_EINVAL, "tt_tree_load: null argument");
+    *out = nullptr;
+    Reader r(path);
+    // read_tree (io.cpp:190-230)
+    r.magic(kTreeMagic, "tree file");
+    const uint64_t timespan = r.le<uint64_t>("timespan");
+    const int p = r.le<uint8_t>("tree header");
+    if (p < 2) fail(TT_EIO, "tree header: order must be >= 2");
+    if (p > TT_MAX_ORDER) fail(TT_EIO, "tree header: order above " + std::to_string(TT_MAX_ORDER));
+    tt_config cfg{};
+    cfg.order = p;
+    for (int m = 0; m < p - 1; ++m) cfg.nontemporal[m] = r.extent("tree shape");
+    for (int m = 0; m < p; ++m) cfg.ranks[m] = r.extent("tree ranks");
+    cfg.theta = r.le<double>("tree theta");
+    cfg.max_iters = static_cast<int32_t>(r.le<uint32_t>("als iters"));
+    cfg.tol = r.le<double>("als tol");
+    cfg.seed = r.le<uint64_t>("als seed");
+    const uint64_t stitches = r.le<uint64_t>("stitch count");
+    const uint64_t root = r.le<uint64_t>("root id");
+    const uint64_t count = r.le<uint64_t>("node count");
+    if (count > (uint64_t(1) << 32)) fail(TT_EIO, "implausible node count");
+    struct Rec {
+      HostNode v;
+      std::vector<double> core;
+      std::vector<std::vector<double>> f;  // column-major
+    };
+    std::vector<Rec> recs(static_cast<size_t>(count));
+    for (uint64_t i = 0; i < count; ++i) {
+      Rec& rc = recs[i];
+      HostNode& v = rc.v;
+      v.id = static_cast<Index>(r.le<uint64_t>("node id"));
+      v.begin = static_cast<Index>(r.le<uint64_t>("node range"));
+      v.end = static_cast<Index>(r.le<uint64_t>("node range"));
+      const uint8_t kind = r.le<uint8_t>("node kind");
+      if (kind > 2) fail(TT_EIO, "invalid node kind " + std::to_string(kind));
+      v.kind = kind;
+      v.left = static_cast<Index>(r.le<uint64_t>("node children"));
+      v.right = static_cast<Index>(r.le<uint64_t>("node children"));
+      if (r.le<uint8_t>("node payload flag") != 0) {  // read_factors (io.cpp:103-121)
+        const int fp = r.le<uint8_t>("factor header");
+        if (fp != p) fail(TT_EIO, "factor header: order does not match the tree");
+        Index cd[kMaxP];
+        for (int m = 0; m < p; ++m) cd[m] = r.extent("core dims");
+        rc.core.resize(static_cast<size_t>(prod_range(cd, 0, p)));
+        r.bytes(rc.core.data(), rc.core.size() * sizeof(double), "core payload");
+        rc.f.resize(static_cast<size_t>(p));
+        std::vector<double> rowmajor;
+        for (int m = 0; m < p; ++m) {
+          const Index rows = r.extent("factor rows"), cols = r.extent("factor cols");
+          if (cols != cd[m]) fail(TT_EIO, "factor cols do not match the core dims");
+          if (rows != (m == 0 ? v.end - v.begin : cfg.nontemporal[m - 1]))
+            fail(TT_EIO, "factor rows do not match the node / tree shape");
+          rowmajor.resize(static_cast<size_t>(rows * cols));
+          r.bytes(rowmajor.data(), rowmajor.size() * sizeof(double), "factor payload");
+          rc.f[m].resize(rowmajor.size());
+          for (Index a = 0; a < rows; ++a)
+            for (Index j = 0; j < cols; ++j) rc.f[m][size_t(a + j * rows)] = rowmajor[size_t(a * cols + j)];
+          v.ranks[m] = cols;
+        }
+        v.has_dec = true;
+      }
+    }
+    // optional engine extension: leaf block and raw tail
+    Index B = 1, tail = 0;
+    std::vector<double> tail_buf;
+    char ext[4];
+    if (r.try_bytes(ext, 4)) {
+      if (std::memcmp(ext, kBlockMagic, 4) != 0) fail(TT_EIO, "unexpected trailing bytes after the node table");
+      const uint16_t version = r.le<uint16_t>("block extension");
+      if (version != kFormatVersion) fail(TT_EIO, "unsupported block-extension version");
+      B = r.extent("leaf block");
+      tail = r.extent("tail slices");
+      if (B < 1 || tail >= B) fail(TT_EIO, "invalid leaf block / tail");
+      Index ss = 1;
+      for (int m = 0; m < p - 1; ++m) ss *= cfg.nontemporal[m];
+      tail_buf.resize(static_cast<size_t>(tail * ss));
+      r.bytes(tail_buf.data(), tail_buf.size() * sizeof(double), "tail payload");
+    }
+    cfg.leaf_block = B;
+    cfg.device = device;
+    cfg.flags = flags;
+    tt_tree* raw = nullptr;
+    const tt_status st = tt_tree_create(&cfg, &raw);
+    if (st != TT_OK) fail(st, g_err);
+    std::unique_ptr<tt_tree, void (*)(tt_tree*)> t(raw, tt_tree_destroy);
+    // from_parts (sst.cpp:30-71): ids are creation order 1..n, children exist
+    Index leaves = 0;
+    for (uint64_t i = 0; i < count; ++i) {
+      const HostNode& v = recs[i].v;
+      if (v.id != static_cast<Index>(i + 1)) fail(TT_EIO, "node ids must be 1..n in creation order");
+      if (v.left > static_cast<Index>(count) || v.right > static_cast<Index>(count) || v.left < 0 || v.right < 0)
+        fail(TT_EIO, "node child id out of range");
+      if (v.begin < 0 || v.end <= v.begin || v.end % B != 0 || v.begin % B != 0)
+        fail(TT_EIO, "node range not aligned to the leaf block");
+      if (v.kind == TT_LEAF) ++leaves;
+    }
+    if (root > count) fail(TT_EIO, "root id out of range");
+    if (static_cast<Index>(timespan) != leaves * B + tail) fail(TT_EIO, "timespan does not match the leaves and tail");
+    t->nodes.reserve(static_cast<size_t>(count));
+    for (Rec& rc : recs) {
+      HostNode v = rc.v;
+      v.core = nullptr;
+      for (int m = 0; m < kMaxP; ++m) v.f[m] = nullptr;
+      t->nodes.push_back(v);
+      HostNode& dv = t->nodes.back();
+      if (!dv.has_dec || t->structure_only) continue;
+      for (int m = 0; m < p; ++m)
+        if (dv.ranks[m] > t->clamped(m, dv.length())) fail(TT_EIO, "node rank exceeds the tree's ranks");
+      t->alloc_slots(dv);
+      DeviceGuard g(t->ex->device);
+      cuda_check(cudaMemcpyAsync(dv.core, rc.core.data(), rc.core.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                 t->ex->stream),
+                 "node core upload");
+      for (int m = 0; m < p; ++m)
+        cuda_check(cudaMemcpyAsync(dv.f[m], rc.f[m].data(), rc.f[m].size() * sizeof(double), cudaMemcpyHostToDevice,
+                                   t->ex->stream),
+                   "node factor upload");
+      t->ex->sync();  // host staging buffers are freed per node
+    }
+    t->root = static_cast<Index>(root);
+    t->timespan = static_cast<Index>(timespan);
+    t->leaves = leaves;
+    t->stitch_count = static_cast<Index>(stitches);
+    t->last_touches = 0;
+    if (tail > 0 && !t->structure_only) {
+      DeviceGuard g(t->ex->device);
+      cuda_check(cudaMemcpy(t->tail.p, tail_buf.data(), tail_buf.size() * sizeof(double), cudaMemcpyHostToDevice),
+                 "tail upload");
+    }
+    *out = t.release();
+  });
+}
+
+tt_status tt_tree_config(const tt_tree* t, tt_config* out) {
+  return guarded([&] {
+    if (!t || !out) fail(TT_EINVAL, "tt_tree_config: null argument");
+    *out = t->cfg;
+  });
+}
+
+tt_status tt_tensor_write(const char* path, int32_t p, const int64_t* dims, const double* data) {
+  return guarded([&] {  // write_tensor (io.cpp:124-133)
+    if (!path || !dims || p < 1 || p > 255) fail(TT_EINVAL, "tt_tensor_write: bad argument");
+    Index n = 1;
+    for (int m = 0; m < p; ++m) {
+      if (dims[m] < 0) fail(TT_EINVAL, "tt_tensor_write: negative extent");
+      n *= dims[m];
+    }
+    if (n > 0 && !data) fail(TT_EINVAL, "tt_tensor_write: null data");
+    Writer w(path);
+    w.bytes(kTensorMagic, 4);
+    w.le<uint16_t>(kFormatVersion);
+    w.le<uint8_t>(static_cast<uint8_t>(p));
+    for (int m = 0; m < p; ++m) w.le<uint64_t>(static_cast<uint64_t>(dims[m]));
+    w.bytes(data, static_cast<size_t>(n) * sizeof(double));
+    w.close();
+  });
+}
+
+tt_status tt_tensor_read(const char* path, int32_t* p, int64_t* dims, double* data) {
+  return guarded([&] {  // read_tensor (io.cpp:135-145)
+    if (!path || !p || !dims) fail(TT_EINVAL, "tt_tensor_read: null argument");
+    Reader r(path);
+    r.magic(kTensorMagic, "tensor file");
+    const int order = r.le<uint8_t>("tensor header");
+    if (order < 1) fail(TT_EIO, "tensor header: order must be >= 1");
+    if (order > TT_TENSOR_MAX_ORDER) fail(TT_EIO, "tensor header: order above TT_TENSOR_MAX_ORDER");
+    *p = order;
+    Index n = 1;
+    for (int m = 0; m < order; ++m) {
+      dims[m] = r.extent("tensor dims");
+      n *= dims[m];
+    }
+    if (data) r.bytes(data, static_cast<size_t>(n) * sizeof(double), "tensor payload");
+  });
+}
+
+}  // extern "C"

@@ -75,6 +75,11 @@ SIGNATURES = {
     "tt_recall": (C.c_int, [vp, i64, i64, C.c_double, C.POINTER(TTHit), i64, i64ptr]),
     "tt_query_batch": (C.c_int, [vp, C.POINTER(TTRange), i64, C.c_double, C.POINTER(TTQueryOut), C.c_int]),
     "tt_last_timing": (C.c_int, [vp, dptr]),
+    "tt_tree_save": (C.c_int, [vp, C.c_char_p]),
+    "tt_tree_config": (C.c_int, [vp, C.POINTER(TTConfig)]),
+    "tt_tree_load": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.POINTER(vp)]),
+    "tt_tensor_write": (C.c_int, [C.c_char_p, C.c_int32, i64ptr, dptr]),
+    "tt_tensor_read": (C.c_int, [C.c_char_p, C.POINTER(C.c_int32), i64ptr, dptr]),
     "tt_tucker_als": (C.c_int, [dptr, C.c_int32, i64ptr, i64ptr, C.c_int32, C.c_double, C.c_uint64, C.c_int32,
                                 C.POINTER(vp)]),
     "tt_stitch": (C.c_int, [C.c_int32, C.c_int32, i64ptr, i64ptr, C.POINTER(dptr), C.POINTER(dptr), i64ptr,
@@ -129,6 +134,10 @@ class CudaError(TuckTreeError, RuntimeError):
     pass
 
 
+class IOError_(TuckTreeError, RuntimeError):
+    """std::runtime_error from the reference's I/O layer (io.cpp:19)."""
+
+
 def _check(code: int):
     if code == 0:
         return
@@ -137,6 +146,8 @@ def _check(code: int):
         raise InvalidArgument(msg)
     if code == 2:
         raise LogicError(msg)
+    if code == 3:
+        raise IOError_(msg)
     if code == 4:
         raise CudaError(msg)
     raise TuckTreeError(f"status {code}: {msg}")
@@ -298,6 +309,29 @@ class StreamSegmentTree:
         self._h = vp()
         _check(lib().tt_tree_create(C.byref(cfg), C.byref(self._h)))
 
+    # -- persistence (io.hpp:21-31) -------------------------------------------
+    def save(self, path: str):
+        """write_tree_file: the reference's SST1 container (+ TTB1 extension for B > 1)."""
+        _check(lib().tt_tree_save(self._h, os.fsencode(path)))
+
+    @classmethod
+    def load(cls, path: str, device: int = 0, structure_only: bool = False) -> "StreamSegmentTree":
+        """read_tree_file: rebuilds the tree (node payloads uploaded to `device`)."""
+        h = vp()
+        _check(lib().tt_tree_load(os.fsencode(path), device, FLAG_STRUCTURE_ONLY if structure_only else 0,
+                                  C.byref(h)))
+        self = cls.__new__(cls)
+        self._h = h
+        self.device = device
+        cfg = TTConfig()
+        _check(lib().tt_tree_config(h, C.byref(cfg)))
+        p = cfg.order
+        self.nontemporal = tuple(int(cfg.nontemporal[m]) for m in range(p - 1))
+        self.ranks = tuple(int(cfg.ranks[m]) for m in range(p))
+        self.theta, self.leaf_block = cfg.theta, int(cfg.leaf_block)
+        self.max_iters, self.tol, self.seed = int(cfg.max_iters), cfg.tol, int(cfg.seed)
+        return self
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
@@ -431,6 +465,23 @@ class StreamSegmentTree:
     def range_query_detailed(self, ts: int, te: int, theta: Optional[float] = None) -> QueryResult:
         hits = self.recall(ts, te, theta)
         return QueryResult(self.range_query(ts, te, theta), hits)
+
+
+def write_tensor(path: str, x: np.ndarray):
+    """write_tensor_file: the reference's TTS1 container (io.hpp:11-19)."""
+    a = np.ascontiguousarray(x, dtype=np.float64)
+    dims, dp = _i(a.shape)
+    _check(lib().tt_tensor_write(os.fsencode(path), a.ndim, dp, _d(a)))
+
+
+def read_tensor(path: str) -> np.ndarray:
+    """read_tensor_file (io.hpp:11-19)."""
+    p = C.c_int32(0)
+    dims, dp = _i(np.zeros(32, dtype=np.int64))
+    _check(lib().tt_tensor_read(os.fsencode(path), C.byref(p), dp, None))
+    out = np.empty(tuple(int(d) for d in dims[:p.value]), dtype=np.float64)
+    _check(lib().tt_tensor_read(os.fsencode(path), C.byref(p), dp, _d(out)))
+    return out
 
 
 def kernel_launches() -> int:

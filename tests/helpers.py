@@ -131,3 +131,56 @@ def min_hit_set_size_naive(nodes, ts, te, theta):
         if ok and cur == te:
             best = len(chosen) if best is None else min(best, len(chosen))
     return -1 if best is None else best
+
+
+# ---------------------------------------------------------------- SST1 / TTS1
+def parse_sst1(path):
+    """Independent parser of the reference's SST1 tree container
+    (/root/reference/proj/core/include/tucktree/io.hpp:21-29) plus the engine's
+    TTB1 leaf-block extension. Returns (header dict, node list, extension)."""
+    import struct
+
+    b = open(path, "rb").read()
+    pos = 0
+
+    def take(fmt):
+        nonlocal pos
+        v = struct.unpack_from("<" + fmt, b, pos)
+        pos += struct.calcsize("<" + fmt)
+        return v if len(v) > 1 else v[0]
+
+    assert b[:4] == b"SST1"
+    pos = 4
+    hdr = {"version": take("H"), "timespan": take("Q"), "p": take("B")}
+    p = hdr["p"]
+    hdr["nontemporal"] = [take("Q") for _ in range(p - 1)]
+    hdr["ranks"] = [take("Q") for _ in range(p)]
+    hdr["theta"], hdr["max_iters"], hdr["tol"], hdr["seed"] = take("d"), take("I"), take("d"), take("Q")
+    hdr["stitch_count"], hdr["root"], hdr["count"] = take("Q"), take("Q"), take("Q")
+    nodes = []
+    for _ in range(hdr["count"]):
+        v = {"id": take("Q"), "begin": take("Q"), "end": take("Q"), "kind": take("B"), "left": take("Q"),
+             "right": take("Q"), "has_dec": take("B")}
+        if v["has_dec"]:
+            q = take("B")
+            cd = [take("Q") for _ in range(q)]
+            n = int(np.prod(cd))
+            core = np.frombuffer(b, dtype="<f8", count=n, offset=pos).reshape(cd)
+            pos += 8 * n
+            fac = []
+            for _m in range(q):
+                rows, cols = take("Q"), take("Q")
+                fac.append(np.frombuffer(b, dtype="<f8", count=rows * cols, offset=pos).reshape(rows, cols))
+                pos += 8 * rows * cols
+            v["core"], v["factors"] = core, fac
+        nodes.append(v)
+    ext = None
+    if pos < len(b):
+        assert b[pos:pos + 4] == b"TTB1"
+        pos += 4
+        ext = {"version": take("H"), "leaf_block": take("Q"), "tail": take("Q")}
+        n = ext["tail"] * int(np.prod(hdr["nontemporal"]))
+        ext["tail_data"] = np.frombuffer(b, dtype="<f8", count=n, offset=pos)
+        pos += 8 * n
+    assert pos == len(b)
+    return hdr, nodes, ext
