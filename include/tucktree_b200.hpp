@@ -147,6 +147,9 @@ class StreamSegmentTree {  // sst.hpp:54-105
   StreamSegmentTree& operator=(const StreamSegmentTree&) = delete;
   StreamSegmentTree(StreamSegmentTree&& o) noexcept : cfg_(std::move(o.cfg_)), h_(std::exchange(o.h_, nullptr)) {}
 
+  // Adopts a handle (read_tree_file).
+  StreamSegmentTree(tt_tree* h, TreeConfig cfg) : cfg_(std::move(cfg)), h_(h) {}
+
   // One or more row-major slices from host memory (n = 1: one append).
   void append(const double* slices, Index n = 1) { check(tt_append(h_, slices, n, TT_MEM_HOST)); }
   // Burst append straight from device memory.
@@ -339,6 +342,46 @@ inline TuckerFactors stitch(const std::vector<TuckerFactors>& parts, const std::
     trace->objective.assign(tt_factors_objective(h), tt_factors_objective(h) + tt_factors_sweeps(h));
   }
   return detail::take(h);
+}
+
+// ---- persistence (io.hpp:15-31): SST1 trees, TTS1 tensors -------------------
+inline void write_tree_file(const std::string& path, const StreamSegmentTree& tree) {
+  check(tt_tree_save(tree.handle(), path.c_str()));
+}
+
+inline StreamSegmentTree read_tree_file(const std::string& path, int device = 0, int flags = 0) {
+  tt_tree* h = nullptr;
+  check(tt_tree_load(path.c_str(), device, flags, &h));
+  tt_config c{};
+  check(tt_tree_config(h, &c));
+  TreeConfig cfg;
+  for (int m = 0; m + 1 < c.order; ++m) cfg.nontemporal.push_back(c.nontemporal[m]);
+  for (int m = 0; m < c.order; ++m) cfg.ranks.push_back(c.ranks[m]);
+  cfg.theta = c.theta;
+  cfg.als.max_iters = c.max_iters;
+  cfg.als.tol = c.tol;
+  cfg.als.seed = c.seed;
+  cfg.leaf_block = c.leaf_block;
+  cfg.device = c.device;
+  cfg.flags = c.flags;
+  return StreamSegmentTree(h, std::move(cfg));
+}
+
+inline void write_tensor_file(const std::string& path, const std::vector<Index>& dims, const double* data) {
+  check(tt_tensor_write(path.c_str(), static_cast<int32_t>(dims.size()), dims.data(), data));
+}
+
+// Returns the payload (row-major) and sets dims.
+inline std::vector<double> read_tensor_file(const std::string& path, std::vector<Index>& dims) {
+  int32_t p = 0;
+  int64_t d[TT_TENSOR_MAX_ORDER] = {};
+  check(tt_tensor_read(path.c_str(), &p, d, nullptr));
+  dims.assign(d, d + p);
+  Index n = 1;
+  for (Index v : dims) n *= v;
+  std::vector<double> out(static_cast<size_t>(n));
+  check(tt_tensor_read(path.c_str(), &p, d, out.data()));
+  return out;
 }
 
 }  // namespace tucktree_b200

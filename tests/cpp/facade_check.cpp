@@ -60,7 +60,24 @@ int main(int argc, char** argv) {
     threw = true;
   }
   CHECK(threw);
+  {  // TTS1 round trip through the facade (host I/O only)
+    const std::vector<double> x = {1.5, -2.0, 3.25, 4.0, 5.5, -6.0};
+    write_tensor_file("facade_check.tts", {3, 2}, x.data());
+    std::vector<Index> dims;
+    const std::vector<double> y = read_tensor_file("facade_check.tts", dims);
+    CHECK((dims == std::vector<Index>{3, 2}) && y == x);
+    threw = false;
+    try {
+      read_tensor_file("does_not_exist.tts", dims);
+    } catch (const std::runtime_error&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
   if (gpu) {
+    write_tree_file("facade_check.sst", tree);
+    const StreamSegmentTree back = read_tree_file("facade_check.sst");
+    CHECK(back.timespan() == 9 && back.stitch_count() == tree.stitch_count() && back.validate().empty());
     const auto rs = range_query_batch(tree, {{0, 9}, {1, 6}, {3, 4}});
     CHECK(rs.size() == 3 && rs[0].dim(0) == 9 && rs[1].dim(0) == 5 && rs[2].dim(0) == 1);
     const TuckerFactors leaf = tree.decomposition(h[1].node);

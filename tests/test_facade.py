@@ -21,12 +21,12 @@ def _compile(tmp_path):
 
 def test_facade_structure(tmp_path):
     exe = _compile(tmp_path)
-    r = subprocess.run([exe], capture_output=True, text=True)
+    r = subprocess.run([exe], capture_output=True, text=True, cwd=tmp_path)
     assert r.returncode == 0, r.stdout + r.stderr
 
 
 @pytest.mark.gpu
 def test_facade_gpu(tmp_path):
     exe = _compile(tmp_path)
-    r = subprocess.run([exe, "gpu"], capture_output=True, text=True)
+    r = subprocess.run([exe, "gpu"], capture_output=True, text=True, cwd=tmp_path)
     assert r.returncode == 0, r.stdout + r.stderr
