@@ -213,6 +213,14 @@ tt_status tt_stitch(int32_t nparts, int32_t p, const int64_t* part_dims, const i
                     const double* const* cores, const double* const* factors, const int64_t* ranks,
                     int32_t max_iters, double tol, uint64_t seed, int32_t device, tt_factors** out);
 
+/* brute_force_range(series, ts, te, ranks, cfg) for a batch of ranges: the
+ * series (row-major, dims[0] = T) in host or device memory; one tucker_als per
+ * range, all in one launch. outs[i] receives range i's factors.
+ *                                                      baseline.cpp:67-75 */
+tt_status tt_brute_force_batch(const double* series, tt_mem where, int32_t p, const int64_t* dims,
+                               const int64_t* ranks, const tt_range* ranges, int64_t n, int32_t max_iters, double tol,
+                               uint64_t seed, int32_t device, tt_factors** outs);
+
 /* partial_hit_factors(stored, begin, end) on device.       stitch.hpp:15 */
 tt_status tt_partial_hit(int32_t p, const int64_t* dims, const int64_t* ranks, const double* core,
                          const double* const* factors, int64_t begin, int64_t end, int32_t device, tt_factors** out);

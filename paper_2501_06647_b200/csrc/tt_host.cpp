@@ -1640,6 +1640,99 @@ tt_status tt_tucker_als(const double* x, int32_t p, const int64_t* dims, const i
   });
 }
 
+tt_status tt_brute_force_batch(const double* series, tt_mem where, int32_t p, const int64_t* dims,
+                               const int64_t* ranks, const tt_range* ranges, int64_t n, int32_t max_iters, double tol,
+                               uint64_t seed, int32_t device, tt_factors** outs) {
+  return guarded([&] {  // brute_force_range (baseline.cpp:67-75), batched: one leaf-kernel CTA per range
+    if (!series || !dims || !ranks || (n > 0 && (!ranges || !outs))) fail(TT_EINVAL, "null argument");
+    if (n < 0) fail(TT_EINVAL, "brute_force: negative range count");
+    if (p < 2 || p > TT_MAX_ORDER) fail(TT_EINVAL, "brute_force: order must be in [2, 8]");
+    if (max_iters < 1) fail(TT_EINVAL, "tucker_als: max_iters must be >= 1");
+    if (tol <= 0.0) fail(TT_EINVAL, "tucker_als: tol must be > 0");
+    for (int m = 0; m < p; ++m) {
+      if (dims[m] < 1) fail(TT_EINVAL, "Shape: all dims must be >= 1");
+      if (ranks[m] < 1) fail(TT_EINVAL, "clamp_ranks: ranks must be >= 1");
+      if (ranks[m] > 32) fail(TT_EINVAL, "tucker_als: ranks above 32 are not supported by this build");
+    }
+    for (int64_t i = 0; i < n; ++i) {
+      outs[i] = nullptr;
+      if (ranges[i].ts < 0 || ranges[i].ts >= ranges[i].te || ranges[i].te > dims[0])
+        fail(TT_EINVAL, "brute_force_range: invalid range");  // baseline.cpp:69-71
+    }
+    if (n == 0) return;
+    StandaloneCtx& c = standalone(device);
+    Exec& ex = *c.ex;
+    DeviceGuard g(device);
+    Index d[kMaxP], rq[kMaxP];
+    for (int m = 0; m < kMaxP; ++m) {
+      d[m] = m < p ? dims[m] : 1;
+      rq[m] = m < p ? ranks[m] : 1;
+    }
+    const Index ss = prod_range(d, 1, p);
+    DevBuf bx;
+    const double* dx = series;
+    if (where == TT_MEM_HOST) dx = upload(bx, series, static_cast<size_t>(d[0] * ss), ex.stream);
+    InitCache init;  // tucker_als draws its init factors per range length (tucker.cpp:26-37)
+    init.p = p;
+    for (int m = 0; m < p; ++m) {
+      init.d[m] = d[m];
+      init.req[m] = rq[m];
+    }
+    init.seed = seed;
+    std::vector<LeafDesc> descs(static_cast<size_t>(n));
+    std::vector<Index> ws(static_cast<size_t>(n));
+    std::vector<Index> lens(static_cast<size_t>(n));
+    size_t need = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      Index dl[kMaxP], rc[kMaxP];
+      std::copy(d, d + kMaxP, dl);
+      dl[0] = lens[i] = ranges[i].te - ranges[i].ts;
+      clamp_ranks(p, dl, rq, rc);
+      need += static_cast<size_t>(prod_range(rc, 0, p)) + 32;
+      for (int m = 0; m < p; ++m) need += static_cast<size_t>(dl[m] * rc[m]) + 16;
+      ws[i] = leaf_ws_layout(p, dl[0], d, rq).total;
+    }
+    DevBuf bout;
+    bout.ensure(need * sizeof(double));
+    double* cur = bout.as<double>();
+    for (int64_t i = 0; i < n; ++i) {
+      LeafDesc& dsc = descs[i];
+      Index dl[kMaxP], rc[kMaxP];
+      std::copy(d, d + kMaxP, dl);
+      dl[0] = lens[i];
+      clamp_ranks(p, dl, rq, rc);
+      const auto& iv = init.leaf_init(lens[i], ex.stream);
+      dsc.x = dx + ranges[i].ts * ss;
+      dsc.len = lens[i];
+      for (int m = 0; m < p; ++m) {
+        dsc.init[m] = iv[m]->as<double>();
+        dsc.out_f[m] = cur;
+        cur += dl[m] * rc[m] + 16;
+      }
+      dsc.out_core = cur;
+      cur += prod_range(rc, 0, p) + 32;
+    }
+    Params prm = make_params(p, d, rq, max_iters, tol);
+    const auto st = run_leaf_batch(ex, prm, descs, ws);
+    for (int64_t i = 0; i < n; ++i) {
+      auto f = std::make_unique<tt_factors>();
+      f->p = p;
+      for (int m = 0; m < p; ++m) {
+        f->dims[m] = m == 0 ? lens[i] : d[m];
+        f->ranks[m] = st[i].k[m];
+      }
+      f->core = download(descs[i].out_core, static_cast<size_t>(prod_range(f->ranks, 0, p)), ex.stream);
+      for (int m = 0; m < p; ++m)
+        f->f.push_back(download(descs[i].out_f[m], static_cast<size_t>(f->dims[m] * f->ranks[m]), ex.stream));
+      f->objective = st[i].objective;
+      f->sweeps = st[i].sweeps;
+      f->converged = st[i].converged;
+      outs[i] = f.release();
+    }
+    ex.sync();
+  });
+}
+
 tt_status tt_stitch(int32_t nparts, int32_t p, const int64_t* part_dims, const int64_t* part_ranks,
                     const double* const* cores, const double* const* factors, const int64_t* ranks, int32_t max_iters,
                     double tol, uint64_t seed, int32_t device, tt_factors** out) {

@@ -76,6 +76,8 @@ SIGNATURES = {
     "tt_query_batch": (C.c_int, [vp, C.POINTER(TTRange), i64, C.c_double, C.POINTER(TTQueryOut), C.c_int]),
     "tt_last_timing": (C.c_int, [vp, dptr]),
     "tt_tree_save": (C.c_int, [vp, C.c_char_p]),
+    "tt_brute_force_batch": (C.c_int, [dptr, C.c_int, C.c_int32, i64ptr, i64ptr, C.POINTER(TTRange), i64, C.c_int32,
+                                       C.c_double, C.c_uint64, C.c_int32, C.POINTER(vp)]),
     "tt_tree_config": (C.c_int, [vp, C.POINTER(TTConfig)]),
     "tt_tree_load": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.POINTER(vp)]),
     "tt_tensor_write": (C.c_int, [C.c_char_p, C.c_int32, i64ptr, dptr]),
@@ -465,6 +467,46 @@ class StreamSegmentTree:
     def range_query_detailed(self, ts: int, te: int, theta: Optional[float] = None) -> QueryResult:
         hits = self.recall(ts, te, theta)
         return QueryResult(self.range_query(ts, te, theta), hits)
+
+
+def brute_force_batch(x: np.ndarray, ranges, ranks: Sequence[int], max_iters: int = 20, tol: float = 0.01,
+                      seed: int = kDefaultSeed, device: int = 0) -> list:
+    """brute_force_range (baseline.cpp:67-75) for many ranges of one series: a
+    tucker_als per range on the device, all ranges in one launch."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    rr = (TTRange * max(len(ranges), 1))()
+    for i, (a, b) in enumerate(ranges):
+        rr[i].ts, rr[i].te = int(a), int(b)
+    dims, dp = _i(x.shape)
+    r, rp = _i(ranks)
+    if len(ranks) != x.ndim:
+        raise InvalidArgument("brute_force_range: one rank per mode required")
+    hs = (vp * max(len(ranges), 1))()
+    _check(lib().tt_brute_force_batch(_d(x), TT_MEM_HOST, x.ndim, dp, rp, rr, len(ranges), max_iters, tol, seed,
+                                      device, hs))
+    return [_take_factors(hs[i]) for i in range(len(ranges))]
+
+
+def brute_force_range(x: np.ndarray, ts: int, te: int, ranks: Sequence[int], max_iters: int = 20, tol: float = 0.01,
+                      seed: int = kDefaultSeed, device: int = 0) -> TuckerFactors:
+    """brute_force_range (baseline.cpp:67-75): tucker_als of X[ts:te) on the device."""
+    return brute_force_batch(x, [(ts, te)], ranks, max_iters, tol, seed, device)[0]
+
+
+def relative_error(x: np.ndarray, candidate: TuckerFactors, reference: TuckerFactors) -> float:
+    """relative_error (tucker.cpp:121-143), measurement side: ||X - Y_A|| / ||X - Y_ALS|| - 1,
+    0/0 -> 0, x/0 -> +inf."""
+    def residual(f):
+        rec = f.core
+        for m, u in enumerate(f.factors):
+            rec = np.moveaxis(np.tensordot(u, rec, axes=(1, m)), 0, m)
+        if rec.shape != x.shape:
+            raise InvalidArgument("relative_error: reconstruction shape mismatch")
+        return float(np.sqrt(np.sum((x - rec) ** 2)))
+    cand, ref = residual(candidate), residual(reference)
+    if ref == 0.0:
+        return 0.0 if cand == 0.0 else float("inf")
+    return cand / ref - 1.0
 
 
 def write_tensor(path: str, x: np.ndarray):

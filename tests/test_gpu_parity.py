@@ -313,3 +313,34 @@ def test_query_outputs_pinned_host_equal_pageable(E):
         for m in range(p):
             got = fs[m].numpy()[: rows[m] * k[m]].reshape(k[m], rows[m]).T
             assert np.array_equal(got, want[i].factors[m])
+
+
+# ------------------------------------------------------------------ brute force + accuracy metric
+def test_brute_force_batch_matches_oracle(E):
+    # brute_force_range (baseline.cpp:67-75): tucker_als of X[ts:te), many ranges in one launch
+    x = _series((300, 24, 8), (4, 3, 3), 0.05, 21)
+    ranges = [(0, 300), (5, 6), (17, 90), (100, 229), (298, 300), (1, 64), (3, 4)]
+    got = E.brute_force_batch(x, ranges, (5, 4, 3))
+    for (ts, te), g in zip(ranges, got):
+        want = O.tucker_als(x[ts:te], [5, 4, 3])
+        assert g.sweeps == len(want.objective), (ts, te)
+        assert_factors_match(x[ts:te], g, want, f"brute force [{ts},{te})")
+
+
+def test_relative_error_metric_matches_oracle(E):
+    # the paper's accuracy metric (tucker.cpp:121-143): tree answer vs brute force on the same range
+    series = _series((512, 32, 16), (5, 5, 5), 0.3, 5)
+    ora = O.Tree(series.shape[1:], (5, 5, 5), leaf_block=64)
+    eng = E.StreamSegmentTree(series.shape[1:], (5, 5, 5), leaf_block=64)
+    ora.append(series)
+    eng.append(series)
+    qs = _ranges(512, 10, 7, minlen=8)
+    brute = E.brute_force_batch(series, qs, (5, 5, 5))
+    for (ts, te), got, bf in zip(qs, eng.range_query_batch(qs), brute):
+        x = series[ts:te]
+        want = ora.range_query(ts, te)
+        want_bf = O.tucker_als(x, [5, 5, 5])
+        rel_e = E.relative_error(x, got, bf)
+        rel_o = E.relative_error(x, want, want_bf)
+        assert abs(rel_e - rel_o) <= 1e-6, (ts, te, rel_e, rel_o)
+        assert rel_e >= -1e-9  # ALS on the raw range is at least as accurate here

@@ -102,3 +102,22 @@ def test_missing_files_raise_io_error(tmp_path):
         E.read_tensor(str(tmp_path / "nope.tts"))
     with pytest.raises(E.tucktree.IOError_):
         E.StreamSegmentTree.load(str(tmp_path / "nope.sst"), structure_only=True)
+
+
+def test_relative_error_edge_cases():
+    # tucker.cpp:138-141: 0/0 -> 0, x/0 -> +inf
+    x = np.zeros((2, 2, 2))
+    zero = E.TuckerFactors(np.zeros((1, 1, 1)), [np.zeros((2, 1))] * 3)
+    one = E.TuckerFactors(np.ones((1, 1, 1)), [np.ones((2, 1)) / np.sqrt(2)] * 3)
+    assert E.relative_error(x, zero, zero) == 0.0
+    assert E.relative_error(x, one, zero) == float("inf")
+    with pytest.raises(ValueError):
+        E.relative_error(np.zeros((3, 2, 2)), zero, zero)
+
+
+def test_brute_force_validates_ranges_before_device_work():
+    x = np.zeros((10, 3, 2))
+    for bad in [(-1, 3), (4, 4), (2, 11)]:
+        with pytest.raises(ValueError):
+            E.brute_force_batch(x, [bad], (2, 2, 2))
+    assert E.brute_force_batch(x, [], (2, 2, 2)) == []
