@@ -355,48 +355,63 @@ __device__ __noinline__ bool cholqr_pass_k(double* W, int64_t rows, double* smal
   return true;
 }
 
-// Y (cols x K) = A^T U with A(i, c) = P[offc[c] + i*inner]: warps split the
-// rows, each lane keeps up to 16 outputs in registers (row-outer loop, so the
-// loads of a row are independent), partials reduced through shared memory.
+// Y (cols x K) = A^T U with A(i, c) = P[offc[c] + i*inner]. Register-blocked:
+// a thread owns an 8-column block of A times a 2-column block of U (16
+// accumulators; 10 loads feed 16 FMAs per row), the blocks are replicated over
+// row groups, and the row-group partial sums are reduced through shared memory.
 template <int K>
 __device__ __noinline__ void unfold_At_U_k(const double* __restrict__ P, const int* __restrict__ offc, int64_t rows,
                                            int64_t inner, int cols, const double* __restrict__ U,
                                            double* __restrict__ Y, double* part) {
-  constexpr int OPL = 16;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nw = int(blockDim.x >> 5);
+  constexpr int CB = 8;
+  constexpr int JB = K < 2 ? K : 2;
+  constexpr int NJB = (K + JB - 1) / JB;
   const int ne = cols * K;
-  const int64_t chunk = (rows + nw - 1) / nw;
-  const int64_t i0 = warp * chunk, i1 = imin(rows, i0 + chunk);
-  for (int e0 = 0; e0 < ne; e0 += 32 * OPL) {
-    double acc[OPL];
-    int oc[OPL], oj[OPL];
+  const int ncb = (cols + CB - 1) / CB;
+  const int nblk = ncb * NJB;  // <= 64: cols * K <= kSiMaxYK
+  int rg = int(blockDim.x) / nblk;
+  const int cap = si_base() / ne;
+  if (rg > cap) rg = cap;
+  if (rg < 1) rg = 1;
+  const int t = threadIdx.x;
+  const int blk = t % nblk, g = t / nblk;
+  if (g < rg) {
+    const int c0 = (blk % ncb) * CB, j0 = (blk / ncb) * JB;
+    const int64_t chunk = (rows + rg - 1) / rg;
+    const int64_t i0 = g * chunk, i1 = imin(rows, i0 + chunk);
+    int oc[CB];
 #pragma unroll
-    for (int u = 0; u < OPL; ++u) {
-      const int e = e0 + lane + 32 * u;
-      const int ee = e < ne ? e : 0;
-      oc[u] = offc[ee % cols];
-      oj[u] = (ee / cols) * int(rows);
-      acc[u] = 0.0;
-    }
-    const int nu = imin(OPL, (ne - e0 - lane + 31) / 32);
+    for (int u = 0; u < CB; ++u) oc[u] = offc[c0 + u < cols ? c0 + u : 0];
+    const double* Ub[JB];
+#pragma unroll
+    for (int v = 0; v < JB; ++v) Ub[v] = U + int64_t(j0 + v < K ? j0 + v : 0) * rows;
+    double acc[CB][JB];
+#pragma unroll
+    for (int u = 0; u < CB; ++u)
+#pragma unroll
+      for (int v = 0; v < JB; ++v) acc[u][v] = 0.0;
     for (int64_t i = i0; i < i1; ++i) {
       const double* Pi = P + i * inner;
-      const double* Ui = U + i;
+      double a[CB], b[JB];
 #pragma unroll
-      for (int u = 0; u < OPL; ++u)
-        if (u < nu) acc[u] = fma(Pi[oc[u]], Ui[oj[u]], acc[u]);
+      for (int u = 0; u < CB; ++u) a[u] = Pi[oc[u]];
+#pragma unroll
+      for (int v = 0; v < JB; ++v) b[v] = Ub[v][i];
+#pragma unroll
+      for (int u = 0; u < CB; ++u)
+#pragma unroll
+        for (int v = 0; v < JB; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
     }
 #pragma unroll
-    for (int u = 0; u < OPL; ++u) {
-      const int e = e0 + lane + 32 * u;
-      if (u < nu && e < ne) part[warp * ne + e] = acc[u];
-    }
+    for (int u = 0; u < CB; ++u)
+#pragma unroll
+      for (int v = 0; v < JB; ++v)
+        if (c0 + u < cols && j0 + v < K) part[g * ne + (c0 + u) + (j0 + v) * cols] = acc[u][v];
   }
   __syncthreads();
   for (int e = threadIdx.x; e < ne; e += blockDim.x) {
     double v = 0.0;
-    for (int w = 0; w < nw; ++w) v += part[w * ne + e];
+    for (int w = 0; w < rg; ++w) v += part[w * ne + e];
     Y[e] = v;  // e = c + j*cols: column-major cols x K
   }
   __syncthreads();
