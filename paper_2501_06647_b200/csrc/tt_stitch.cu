@@ -137,6 +137,68 @@ __device__ bool materialize_u0(int k0, const StitchPart* parts, int s, const dou
 }
 
 // ---------------------------------------------------------------------------
+// S = V^T V for a tall V (rows x K, ld) with many rows (a partial hit's kept
+// temporal rows: up to tens of thousands): every thread keeps all K(K+1)/2
+// upper-triangle sums for its rows (K loads feed K(K+1)/2 FMAs per row, rows
+// strided over the block so each load instruction is coalesced), then a warp
+// butterfly and a shared-memory pass reduce them. `red` holds kWarps*K(K+1)/2
+// doubles.
+template <int K>
+__device__ __noinline__ void gram_long_k(const double* __restrict__ V, int64_t ld, int64_t rows,
+                                         double* __restrict__ G, double* red) {
+  constexpr int NP = K * (K + 1) / 2;
+  double acc[NP];
+#pragma unroll
+  for (int e = 0; e < NP; ++e) acc[e] = 0.0;
+  for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) {
+    double v[K];
+#pragma unroll
+    for (int a = 0; a < K; ++a) v[a] = V[r + a * ld];
+    int e = 0;
+#pragma unroll
+    for (int a = 0; a < K; ++a)
+#pragma unroll
+      for (int b = a; b < K; ++b) {
+        acc[e] = fma(v[a], v[b], acc[e]);
+        ++e;
+      }
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+  for (int e = 0; e < NP; ++e) {
+    const double s = warp_sum(acc[e]);
+    if (l == 0) red[w * NP + e] = s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < NP; e += blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < int(blockDim.x >> 5); ++q) s += red[q * NP + e];
+    int a = 0, rem = e;  // e -> (a, b), upper triangle row-major
+    while (rem >= K - a) {
+      rem -= K - a;
+      ++a;
+    }
+    const int b = a + rem;
+    G[a + b * K] = s;
+    G[b + a * K] = s;
+  }
+  __syncthreads();
+}
+
+__device__ void gram_long(const double* V, int64_t ld, int64_t rows, int k, double* G, double* red) {
+  switch (k) {
+#define TT_CASE(N)                         \
+  case N:                                  \
+    gram_long_k<N>(V, ld, rows, G, red);   \
+    return;
+    TT_CASE(1) TT_CASE(2) TT_CASE(3) TT_CASE(4) TT_CASE(5) TT_CASE(6) TT_CASE(7) TT_CASE(8) TT_CASE(9) TT_CASE(10)
+#undef TT_CASE
+    default:
+      gram_tall(V, ld, rows, k, G);
+  }
+}
+
+// ---------------------------------------------------------------------------
 struct PartView {
   const double* core;
   int64_t rho[kMaxP];
@@ -332,7 +394,7 @@ __global__ void __launch_bounds__(kStitchThreads, kStitchCtas)
       const double* vs = pv.v0 + pv.row0;
       {
         const long long tg = tstart();
-        gram_tall(vs, pv.ld0, pv.len, int(r0), Sp(i));
+        gram_long(vs, pv.ld0, pv.len, int(r0), Sp(i), dsm);
         tstop(sc, kPhGram, tg);
       }
       // ||H x_0 R||^2 = sum_ab S_ab (M0(H) M0(H)^T)_ab
