@@ -367,6 +367,12 @@ __global__ void __launch_bounds__(kStitchThreads, kStitchCtas)
     for (int r = roff[i] + threadIdx.x; r < roff[i + 1]; r += blockDim.x) rt_pp[r] = pp;
   }
   __syncthreads();
+  int longest = -1;  // the part with the most temporal rows (warm starts)
+  for (int i = 0, best = 0; i < s; ++i)
+    if (parts[i].len > best) {
+      best = int(parts[i].len);
+      longest = i;
+    }
   double* Est = ws + lay.E;  // stacked E (R x k0, ld R): U0 = blockdiag(V_sub,i) E
   double* Ast = ws + lay.A;  // stacked A = S E (rows of partial parts)
   double* Cst = ws + lay.C;  // stacked C (R x Q, row-major)
@@ -890,7 +896,17 @@ __global__ void __launch_bounds__(kStitchThreads, kStitchCtas)
           __syncthreads();
           tstop(sc, kPhTtm, tz);
         }
-        llsv_unfold(Z, zo, d[n], zi, kn, D.out_f[n], G, Vg, misc, dsm, sc, k[n], ws + lay.SI);
+        // Warm start of the eigen-iterations: in sweep 0 the factor still holds the
+        // random init; the longest part's own mode-n factor spans nearly the same
+        // subspace and cuts the iterations. The init value of U_n is not used again
+        // (P_in is recomputed below), and the converged top-k vectors do not depend
+        // on the start.
+        int64_t kprev = k[n];
+        if (sweep == 0 && longest >= 0) {
+          kprev = imin(parts[longest].rho[n], k[n]);
+          bcopy(D.out_f[n], parts[longest].v[n], d[n] * kprev);
+        }
+        llsv_unfold(Z, zo, d[n], zi, kn, D.out_f[n], G, Vg, misc, dsm, sc, kprev, ws + lay.SI);
         k[n] = kn;
         gemm_batched(s, [&](int i) { return pm_entry(i, n); }, sc);
       }
