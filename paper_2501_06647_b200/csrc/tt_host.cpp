@@ -377,6 +377,13 @@ std::vector<ProblemStatus> run_leaf_batch(Exec& ex, const Params& prm, std::vect
   return st;
 }
 
+// Launch-order cost model of a stitch problem, in temporal rows: U0
+// materialisation is linear in L, the solver work grows with the part count.
+// (measured at C2: 10000 for the launch order; the DMA wave split, which
+// decides when the end-to-end download starts, prefers 20000)
+constexpr double kPartCost = 10000.0;
+constexpr double kWavePartCost = 20000.0;
+
 std::vector<ProblemStatus> run_stitch_batch(Exec& ex, const Params& prm, std::vector<StitchDesc>& descs_in,
                                             const std::vector<StitchPart>& parts, const std::vector<Index>& ws_sizes) {
   const int n = static_cast<int>(descs_in.size());
@@ -392,7 +399,7 @@ std::vector<ProblemStatus> run_stitch_batch(Exec& ex, const Params& prm, std::ve
   // costs vary ~100x (L and the part count), so LPT order shrinks the tail.
   std::vector<int> perm(static_cast<size_t>(n));
   for (int i = 0; i < n; ++i) perm[i] = i;
-  auto cost = [&](int i) { return double(descs_in[i].L) + 4096.0 * descs_in[i].nparts; };
+  auto cost = [&](int i) { return double(descs_in[i].L) + kPartCost * descs_in[i].nparts; };
   std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return cost(a) > cost(b); });
   std::vector<StitchDesc> descs(static_cast<size_t>(n));
   std::vector<Index> wsz(static_cast<size_t>(n));
@@ -1392,7 +1399,7 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
       for (int64_t i = 0; i < nc; ++i) order[i] = i;
       std::vector<int64_t> wave_end;
       if (dma && nc >= 64) {
-        auto qcost = [&](int64_t i) { return double(descs[i].L) + 4096.0 * descs[i].nparts; };
+        auto qcost = [&](int64_t i) { return double(descs[i].L) + kWavePartCost * descs[i].nparts; };
         std::vector<int64_t> by_cost(order);
         std::stable_sort(by_cost.begin(), by_cost.end(), [&](int64_t x, int64_t y) { return qcost(x) < qcost(y); });
         const int64_t w0 = (nc + 31) / 32;
