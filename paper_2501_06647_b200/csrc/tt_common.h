@@ -162,12 +162,14 @@ TT_HD LeafWs leaf_ws_layout(int p, int64_t len, const int64_t* d, const int64_t*
 }
 
 struct StitchWs {
-  int64_t P, C, S, E, A, E2, G, V, T1, T2, TB1, TB2, Z, WK, HH, SI, misc, total, gram_n;
+  int64_t P, C, S, E, A, G, V, T1, T2, TB1, TB2, Z, WK, HH, SI, misc, total, gram_n;
   int64_t chain;  // per-part stride of the part-batched mode-product chains (TB1/TB2)
   int64_t per_part_P, per_part_C, per_part_S, per_part_E;
 };
 
-// rcx[m] = max(rc[m], max_i rho_im): bound on every intermediate extent.
+// rcx[m] = max(rc[m], max_i rho_im): bound on every intermediate extent. The C, E
+// and A regions hold the parts' stacked temporal rows (R = sum rho_i0 <=
+// nparts*rcx0 rows; C row-major R x Q, E and A column-major R x k0, ld R).
 TT_HD StitchWs stitch_ws_layout(int p, int64_t L, const int64_t* d, const int64_t* req, const int64_t* rho_max,
                                 int nparts) {
   int64_t dd[kMaxP], rc[kMaxP], rcx[kMaxP];
@@ -195,8 +197,7 @@ TT_HD StitchWs stitch_ws_layout(int p, int64_t L, const int64_t* d, const int64_
   w.S = w.C + nparts * w.per_part_C;
   w.E = w.S + nparts * w.per_part_S;
   w.A = w.E + nparts * w.per_part_E;
-  w.E2 = w.A + nparts * w.per_part_E;
-  w.G = w.E2 + nparts * w.per_part_E;
+  w.G = w.A + nparts * w.per_part_E;
   w.V = w.G + g * g;
   w.T1 = w.V + g * g;
   w.T2 = w.T1 + chain;
