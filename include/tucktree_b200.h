@@ -221,7 +221,11 @@ tt_status tt_brute_force_batch(const double* series, tt_mem where, int32_t p, co
                                const int64_t* ranks, const tt_range* ranges, int64_t n, int32_t max_iters, double tol,
                                uint64_t seed, int32_t device, tt_factors** outs);
 
-/* partial_hit_factors(stored, begin, end) on device.       stitch.hpp:15 */
+/* partial_hit_factors(stored, begin, end) on device: thin Householder QR of
+ * the kept temporal rows with the reference sign rule, core <- core x_0 R.
+ * Inputs are host arrays (factors column-major). Range queries do not use it
+ * (partial hits enter their stitch through the metric S = V_sub^T V_sub).
+ *                                                          stitch.hpp:15 */
 tt_status tt_partial_hit(int32_t p, const int64_t* dims, const int64_t* ranks, const double* core,
                          const double* const* factors, int64_t begin, int64_t end, int32_t device, tt_factors** out);
 

@@ -31,6 +31,10 @@ cudaError_t launch_leaf(const Params& prm, const LeafDesc* d_descs, int n, cudaS
 cudaError_t launch_stitch(const Params& prm, const StitchDesc* d_descs, const StitchPart* d_parts, int n,
                           cudaStream_t st);
 cudaError_t launch_copy_segments(const CopySeg* d_segs, int n, cudaStream_t st);
+cudaError_t launch_partial_hit(const double* V0, int64_t ld, int64_t b, int64_t len, int n, const double* core,
+                               int64_t rest, double* W, double* Q, double* R, double* out_core, double* tau,
+                               cudaStream_t st);
+constexpr int kMaxVecHost = 32;  // the kernel's per-thread column vectors (kMaxVec)
 int64_t launches();
 }  // namespace ttb
 
@@ -1846,12 +1850,49 @@ tt_status tt_stitch(int32_t nparts, int32_t p, const int64_t* part_dims, const i
   });
 }
 
-tt_status tt_partial_hit(int32_t, const int64_t*, const int64_t*, const double*, const double* const*, int64_t,
-                         int64_t, int32_t, tt_factors** out) {
-  return guarded([&] {
-    if (out) *out = nullptr;
-    fail(TT_EINVAL, "tt_partial_hit: standalone partial-hit re-factoring is not part of this build; "
-                    "range queries fold partial hits into the stitch (see DESIGN.md)");
+tt_status tt_partial_hit(int32_t p, const int64_t* dims, const int64_t* ranks, const double* core,
+                         const double* const* factors, int64_t begin, int64_t end, int32_t device, tt_factors** out) {
+  return guarded([&] {  // partial_hit_factors (stitch.cpp:36-47) on the device
+    if (!dims || !ranks || !core || !factors || !out) fail(TT_EINVAL, "null argument");
+    *out = nullptr;
+    if (p < 2 || p > TT_MAX_ORDER) fail(TT_EINVAL, "partial_hit_factors: order must be in [2, 8]");
+    for (int m = 0; m < p; ++m) {
+      if (dims[m] < 1 || ranks[m] < 1) fail(TT_EINVAL, "partial_hit_factors: bad factor shape");
+      if (!factors[m]) fail(TT_EINVAL, "null factor");
+    }
+    const Index len0 = dims[0];
+    if (begin < 0 || begin >= end || end > len0) fail(TT_EINVAL, "partial_hit_factors: invalid sub-range");
+    const int n = static_cast<int>(ranks[0]);
+    if (n > kMaxVecHost) fail(TT_EINVAL, "partial_hit_factors: temporal rank above 32");
+    const Index len = end - begin, k = std::min<Index>(len, n);
+    Index rest = 1;
+    for (int m = 1; m < p; ++m) rest *= ranks[m];
+    StandaloneCtx& c = standalone(device);
+    Exec& ex = *c.ex;
+    DeviceGuard g(device);
+    DevBuf bv, bc, bw, bq, br, bo, bt;
+    const double* dv = upload(bv, factors[0], static_cast<size_t>(len0 * n), ex.stream);
+    const double* dc = upload(bc, core, static_cast<size_t>(n * rest), ex.stream);
+    bw.ensure(static_cast<size_t>(len * n) * sizeof(double));
+    bq.ensure(static_cast<size_t>(len * k) * sizeof(double));
+    br.ensure(static_cast<size_t>(k * n) * sizeof(double));
+    bo.ensure(static_cast<size_t>(std::max<Index>(k * rest, 1)) * sizeof(double));
+    bt.ensure(static_cast<size_t>(n) * sizeof(double));
+    cuda_check(launch_partial_hit(dv, len0, begin, len, n, dc, rest, bw.as<double>(), bq.as<double>(),
+                                  br.as<double>(), bo.as<double>(), bt.as<double>(), ex.stream),
+               "partial_hit_kernel launch");
+    auto f = std::make_unique<tt_factors>();
+    f->p = p;
+    for (int m = 0; m < p; ++m) {
+      f->dims[m] = m == 0 ? len : dims[m];
+      f->ranks[m] = m == 0 ? k : ranks[m];
+    }
+    f->core = download(bo.as<double>(), static_cast<size_t>(k * rest), ex.stream);
+    f->f.push_back(download(bq.as<double>(), static_cast<size_t>(len * k), ex.stream));
+    for (int m = 1; m < p; ++m)
+      f->f.emplace_back(factors[m], factors[m] + static_cast<size_t>(dims[m] * ranks[m]));
+    ex.sync();
+    *out = f.release();
   });
 }
 

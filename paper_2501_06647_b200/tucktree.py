@@ -219,6 +219,20 @@ def tucker_als(x: np.ndarray, ranks: Sequence[int], max_iters: int = 20, tol: fl
     return _take_factors(h)
 
 
+def partial_hit_factors(stored, begin: int, end: int, device: int = 0) -> TuckerFactors:
+    """stitch.hpp:15 — rows [begin, end) of a stored decomposition: thin QR of the
+    kept temporal rows (reference sign rule), core <- core x_0 R, on the GPU."""
+    p = len(stored.factors)
+    dims, dp = _i([f.shape[0] for f in stored.factors])
+    rk, rp = _i([f.shape[1] for f in stored.factors])
+    c = np.ascontiguousarray(stored.core, dtype=np.float64).ravel()
+    keep = [np.asfortranarray(f, dtype=np.float64) for f in stored.factors]
+    facs = (dptr * p)(*[_d(f) for f in keep])
+    h = vp()
+    _check(lib().tt_partial_hit(p, dp, rp, _d(c), facs, int(begin), int(end), device, C.byref(h)))
+    return _take_factors(h)
+
+
 def stitch(parts: Sequence, ranks: Sequence[int], max_iters: int = 20, tol: float = 0.01, seed: int = kDefaultSeed,
            device: int = 0) -> TuckerFactors:
     """stitch.hpp:34-36 — ALS on the implied temporal concatenation of the parts, on the GPU."""

@@ -344,3 +344,39 @@ def test_relative_error_metric_matches_oracle(E):
         rel_o = E.relative_error(x, want, want_bf)
         assert abs(rel_e - rel_o) <= 1e-6, (ts, te, rel_e, rel_o)
         assert rel_e >= -1e-9  # ALS on the raw range is at least as accurate here
+
+
+# ------------------------------------------------------------------ partial_hit_factors
+@pytest.mark.parametrize("dims,ranks,b,e,seed", [
+    ([8, 5, 4], [3, 2, 2], 2, 7, 200),       # test_stitch.cpp:49-80 shape
+    ([8, 5, 4], [3, 2, 2], 0, 8, 201),       # whole range: Q = thin_qr(V0)
+    ([300, 7, 5], [10, 4, 3], 40, 290, 202),  # long kept run
+    ([64, 6, 4], [10, 3, 2], 10, 14, 203),   # len < rank: temporal rank shrinks to len
+    ([16, 4, 3, 2], [5, 2, 2, 2], 3, 11, 204),
+])
+def test_partial_hit_matches_oracle(E, dims, ranks, b, e, seed):
+    rng = np.random.default_rng(seed)
+    stored = H.random_tucker(dims, ranks, rng)
+    implied = H.reconstruct(stored.core, stored.factors)
+    got = E.partial_hit_factors(stored, b, e)
+    want = O.partial_hit_factors(stored, b, e)
+    assert [got.rank(m) for m in range(len(dims))] == [want.rank(m) for m in range(len(dims))]
+    assert got.dim(0) == e - b and H.orthonormality_defect(got.factors[0]) <= 1e-10
+    # exact representation of the kept rows (stitch.cpp:36-47)
+    assert np.max(np.abs(H.reconstruct(got.core, got.factors) - implied[b:e])) <= 1e-10
+    # same Q and R as the oracle's Householder QR + sign rule, to rounding
+    assert np.max(np.abs(got.factors[0] - want.factors[0])) <= 1e-9
+    assert np.max(np.abs(got.core - want.core)) <= 1e-9 * max(1.0, np.max(np.abs(want.core)))
+
+
+def test_partial_hit_rank_deficient_rows(E):
+    # kept rows of rank 1 < r: QR of a rank-deficient block is allowed (linalg.cpp:33-43)
+    rng = np.random.default_rng(205)
+    stored = H.random_tucker([12, 4, 3], [3, 2, 2], rng)
+    v = stored.factors[0].copy()
+    v[4:9] = np.outer(rng.standard_normal(5), rng.standard_normal(3))
+    stored.factors[0] = v
+    got = E.partial_hit_factors(stored, 4, 9)
+    implied = H.reconstruct(stored.core, stored.factors)
+    assert np.max(np.abs(H.reconstruct(got.core, got.factors) - implied[4:9])) <= 1e-10
+    assert H.orthonormality_defect(got.factors[0]) <= 1e-10

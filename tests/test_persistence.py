@@ -121,3 +121,12 @@ def test_brute_force_validates_ranges_before_device_work():
         with pytest.raises(ValueError):
             E.brute_force_batch(x, [bad], (2, 2, 2))
     assert E.brute_force_batch(x, [], (2, 2, 2)) == []
+
+
+def test_partial_hit_validates_range_before_device_work():
+    rng = np.random.default_rng(1)
+    stored = E.TuckerFactors(rng.standard_normal((3, 2, 2)),
+                             [np.linalg.qr(rng.standard_normal((d, r)))[0] for d, r in ((8, 3), (5, 2), (4, 2))])
+    for b, e in [(3, 3), (-1, 2), (0, 9)]:
+        with pytest.raises(ValueError):
+            E.partial_hit_factors(stored, b, e)
