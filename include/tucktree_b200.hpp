@@ -344,6 +344,32 @@ inline TuckerFactors stitch(const std::vector<TuckerFactors>& parts, const std::
   return detail::take(h);
 }
 
+// partial_hit_factors (stitch.hpp:15): rows [begin, end) of a stored decomposition.
+inline TuckerFactors partial_hit_factors(const TuckerFactors& stored, Index begin, Index end, int device = 0) {
+  const Index p = stored.order();
+  std::vector<int64_t> dims, ranks;
+  std::vector<const double*> facs;
+  for (Index m = 0; m < p; ++m) {
+    dims.push_back(stored.dim(m));
+    ranks.push_back(stored.rank(m));
+    facs.push_back(stored.factors[static_cast<size_t>(m)].data.data());
+  }
+  tt_factors* h = nullptr;
+  check(tt_partial_hit(static_cast<int32_t>(p), dims.data(), ranks.data(), stored.core.data(), facs.data(), begin, end,
+                       device, &h));
+  return detail::take(h);
+}
+
+// brute_force_range (baseline.hpp): tucker_als of x[ts:te) (x row-major, dims[0] = T) on the device.
+inline TuckerFactors brute_force_range(const double* x, const std::vector<Index>& dims, Index ts, Index te,
+                                       const std::vector<Index>& ranks, const AlsConfig& cfg, int device = 0) {
+  const tt_range r{ts, te};
+  tt_factors* h = nullptr;
+  check(tt_brute_force_batch(x, TT_MEM_HOST, static_cast<int32_t>(dims.size()), dims.data(), ranks.data(), &r, 1,
+                             cfg.max_iters, cfg.tol, cfg.seed, device, &h));
+  return detail::take(h);
+}
+
 // ---- persistence (io.hpp:15-31): SST1 trees, TTS1 tensors -------------------
 inline void write_tree_file(const std::string& path, const StreamSegmentTree& tree) {
   check(tt_tree_save(tree.handle(), path.c_str()));
