@@ -380,3 +380,29 @@ def test_partial_hit_rank_deficient_rows(E):
     implied = H.reconstruct(stored.core, stored.factors)
     assert np.max(np.abs(H.reconstruct(got.core, got.factors) - implied[4:9])) <= 1e-10
     assert H.orthonormality_defect(got.factors[0]) <= 1e-10
+
+
+# ------------------------------------------------------------------ block baseline (baseline.cpp:24-65)
+def test_block_baseline_matches_oracle_composition(E):
+    from paper_2501_06647_b200 import baseline as BL
+
+    series = _series((200, 12, 6), (4, 3, 3), 0.05, 31)
+    b = BL.default_block_size(200)
+    assert b == O.default_block_size(200)
+    idx = BL.build_blocks(series, b, (5, 4, 3))
+    assert len(idx.blocks) == -(-200 // b)
+    for k, blk in enumerate(idx.blocks):
+        lo, hi = k * b, min(200, (k + 1) * b)
+        assert_factors_match(series[lo:hi], blk, O.tucker_als(series[lo:hi], [5, 4, 3]), f"block {k}")
+    for ts, te in [(0, 200), (3, 17), (b, 2 * b), (b - 1, b + 1), (150, 199)]:
+        got = BL.block_range_query(idx, ts, te)
+        parts = []
+        k = ts // b
+        while k * b < te:
+            lo, hi = k * b, min(200, (k + 1) * b)
+            stored = O.tucker_als(series[lo:hi], [5, 4, 3])
+            a, z = max(ts, lo) - lo, min(te, hi) - lo
+            parts.append(stored if (a == 0 and z == hi - lo) else O.partial_hit_factors(stored, a, z))
+            k += 1
+        want = O.stitch(parts, [5, 4, 3])
+        assert_factors_match(series[ts:te], got, want, f"block query [{ts},{te})")

@@ -130,3 +130,20 @@ def test_partial_hit_validates_range_before_device_work():
     for b, e in [(3, 3), (-1, 2), (0, 9)]:
         with pytest.raises(ValueError):
             E.partial_hit_factors(stored, b, e)
+
+
+def test_block_baseline_host_rules():
+    from paper_2501_06647_b200 import baseline as BL
+
+    assert BL.default_block_size(256) == 16 and BL.default_block_size(2033) == 92  # test_baseline.cpp:27-33
+    assert BL.default_block_size(1) == 1
+    for t in (2, 3, 100, 1000, 4096):
+        assert BL.default_block_size(t) == O.default_block_size(t)
+    with pytest.raises(ValueError):
+        BL.default_block_size(0)
+    with pytest.raises(ValueError):
+        BL.build_blocks(np.zeros((10, 2, 2)), 11, (2, 2, 2))
+    idx = BL.BlockIndex(4, 10, (2, 2), (2, 2, 2))
+    for ts, te in [(-1, 3), (5, 5), (2, 11)]:
+        with pytest.raises(ValueError):
+            BL.block_range_query(idx, ts, te)
