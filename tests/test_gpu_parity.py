@@ -406,3 +406,9 @@ def test_block_baseline_matches_oracle_composition(E):
             k += 1
         want = O.stitch(parts, [5, 4, 3])
         assert_factors_match(series[ts:te], got, want, f"block query [{ts},{te})")
+
+
+def test_ranks_above_subspace_iteration_bound(E):
+    # ranks > 16 (BASELINE C5 uses 20) take the Jacobi paths: leaves, stitches and queries
+    series = _series((192, 40, 30), (20, 12, 10), 0.05, 41)
+    _compare_trees(E, series, (20, 20, 20), 32, queries=[(0, 192), (5, 150), (31, 97), (100, 101)])
