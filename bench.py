@@ -284,7 +284,10 @@ def run_engine(args, rank, world, local_rank):
         "data": "synthetic (seeded; " + w.desc + ")",
         "config": {"workload": w.name, "shape": list(w.shape), "ranks": list(w.ranks), "leaf_block": w.leaf_block,
                    "queries_per_step": nq, "slices_per_step": T, "series_bytes": x.nbytes,
-                   "l2": "inputs larger than L2 (591 MB series re-read by every step's build)",
+                   "l2": (f"inputs larger than L2 ({x.nbytes / 1e6:.0f} MB series re-read by every step's build)"
+                          if x.nbytes > 126e6 else
+                          f"series ({x.nbytes / 1e6:.0f} MB) fits the 126 MB L2: no flush between steps, so the "
+                          "build may hit L2 (the C1 line is a parity/latency case, not the headline)"),
                    "step": "full tree build (burst append from HBM) + query batch"},
         "append": {"value": round(sps, 3), "unit": "slices/s", "ms_per_step": round(t_app / K, 4)},
         "phases_ms_per_step": {"append": round(t_app / K, 4), "append_leaf_als": round(t_leaf / K, 4),
