@@ -16,7 +16,10 @@ constexpr int kStitchThreads = 256;  // 2 stitch CTAs per SM (128 threads x 4 CT
 #endif
 constexpr int kStitchCtas = TT_STITCH_CTAS;  // resident stitch CTAs per SM (register budget)
 // stitch kernel dynamic shared memory: 64 KB at 2 CTAs/SM, 55 KB at 3
-constexpr size_t kDynSmem = kStitchCtas >= 3 ? size_t(55) * 1024 : size_t(2) * kEigSmemN * kEigSmemN * sizeof(double);
+#ifndef TT_STITCH_DYN_KB
+#define TT_STITCH_DYN_KB 56  // measured: 56 KB (more L1 at 2 CTAs/SM) beats 64 and 48 by 3%
+#endif
+constexpr size_t kDynSmem = kStitchCtas >= 3 ? size_t(55) * 1024 : size_t(TT_STITCH_DYN_KB) * 1024;
 
 __device__ __forceinline__ unsigned dyn_smem_doubles() {
   unsigned b;
