@@ -57,7 +57,10 @@ TT_HD int64_t stitch_mode_rank(int p, const int64_t* d, const int64_t* rc, const
 struct StreamTile {
   int64_t tw, G, cj;
 };
-constexpr int64_t kStreamTileDoubles = 2560;  // 20 KB per ring stage
+#ifndef TT_STREAM_TILE_DOUBLES
+#define TT_STREAM_TILE_DOUBLES 3072
+#endif
+constexpr int64_t kStreamTileDoubles = TT_STREAM_TILE_DOUBLES;  // 24 KB per ring stage (measured best of 20/24/32 KB at 2 stages)
 TT_HD StreamTile stream_tile(int64_t outer, int64_t d, int64_t inner) {
   StreamTile t;
   t.tw = imin(inner, 256);
