@@ -33,7 +33,10 @@ __device__ __forceinline__ unsigned dyn_smem_doubles() {
 #endif
 constexpr int kStages = TT_LEAF_STAGES;
 constexpr int kTileD = int(kStreamTileDoubles);   // 20 KB per stage
-constexpr int kUStage = 4096;  // U^T staged in shared memory when d*r <= this (32 KB)
+#ifndef TT_USTAGE_DOUBLES
+#define TT_USTAGE_DOUBLES 4096
+#endif
+constexpr int kUStage = TT_USTAGE_DOUBLES;  // U^T staged in shared memory when d*r <= this (32 KB)
 constexpr size_t kLeafDynSmem = size_t(kStages * kTileD + kUStage) * sizeof(double);  // 96 KB
 
 struct Pipe {
