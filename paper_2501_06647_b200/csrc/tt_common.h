@@ -125,8 +125,10 @@ constexpr int kStatusInts = 4 + kMaxP + 17;  // ..., eig calls, Jacobi sweeps, k
 constexpr int64_t kMisc = 2048;
 
 struct LeafWs {
-  int64_t W, B1, B2, G, V, SI, misc, total, gram_n;
+  int64_t W, B1, B2, G, V, SI, misc, xch, total, gram_n;
 };
+// Cross-CTA exchange slots of the cluster leaf kernel (per-CTA partial sums, stop flag).
+constexpr int64_t kXch = 64;
 
 // Subspace-iteration scratch: U/W (rows x k), Y (cols x k), small k x k
 // matrices and the unfolding column-offset table.
@@ -159,7 +161,8 @@ TT_HD LeafWs leaf_ws_layout(int p, int64_t len, const int64_t* d, const int64_t*
   }
   w.SI = w.V + g * g;
   w.misc = w.SI + si_size(maxrows, g, kmax);
-  w.total = w.misc + kMisc + 4 * g;
+  w.xch = w.misc + kMisc + 4 * g;
+  w.total = w.xch + kXch;
   w.total = (w.total + 31) & ~int64_t(31);
   return w;
 }

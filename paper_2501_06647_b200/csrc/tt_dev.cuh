@@ -760,4 +760,9 @@ static __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows,
 
 extern std::atomic<int64_t> g_launches;
 
+// Sets a kernel's dynamic shared-memory cap on the current device, once per
+// (kernel slot, device): the attribute is per device, so a process driving
+// several devices sets it on each. Returns the attribute call's error.
+cudaError_t ensure_dyn_smem(const void* fn, int slot, size_t bytes);
+
 }  // namespace ttb

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -30,6 +31,8 @@ namespace ttb {
 cudaError_t launch_leaf(const Params& prm, const LeafDesc* d_descs, int n, cudaStream_t st);
 cudaError_t launch_stitch(const Params& prm, const StitchDesc* d_descs, const StitchPart* d_parts, int n,
                           cudaStream_t st);
+int leaf_wide_cluster();
+cudaError_t launch_leaf_wide(const Params& prm, const LeafDesc* d_descs, int n, int cs, cudaStream_t st);
 cudaError_t launch_copy_segments(const CopySeg* d_segs, int n, cudaStream_t st);
 cudaError_t launch_partial_hit(const double* V0, int64_t ld, int64_t b, int64_t len, int n, const double* core,
                                int64_t rest, double* W, double* Q, double* R, double* out_core, double* tau,
@@ -182,6 +185,18 @@ struct Arena {
     ci = 0;
     cur = chunks.empty() ? nullptr : static_cast<char*>(chunks[0].first);
     left = chunks.empty() ? 0 : chunks[0].second;
+  }
+  struct Mark {
+    size_t ci;
+    char* cur;
+    size_t left;
+  };
+  Mark mark() const { return Mark{ci, cur, left}; }
+  // Drops every allocation made after `m` (failed appends roll back).
+  void release(const Mark& m) {
+    ci = m.ci;
+    cur = m.cur;
+    left = m.left;
   }
   double* alloc(size_t n_doubles) {
     size_t b = (n_doubles * sizeof(double) + 255) & ~size_t(255);
@@ -350,7 +365,21 @@ std::vector<ProblemStatus> run_leaf_batch(Exec& ex, const Params& prm, std::vect
   ex.d_desc.ensure(sizeof(LeafDesc) * n);
   cuda_check(cudaMemcpyAsync(ex.d_desc.p, descs.data(), sizeof(LeafDesc) * n, cudaMemcpyHostToDevice, ex.stream),
              "upload leaf descriptors");
-  cuda_check(launch_leaf(prm, ex.d_desc.as<LeafDesc>(), n, ex.stream), "leaf_als_kernel launch");
+  // Few problems: one thread-block cluster per problem (leaf_wide_kernel) so a
+  // single streamed leaf or query tail uses 8-16 SMs; wide batches: one CTA
+  // per problem. TT_WIDE=0/1 forces either path (A/B measurement).
+  const int cs = leaf_wide_cluster();
+  bool wide = cs > 0 && prm.p >= 2;
+  if (wide) {
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ex.device);
+    wide = n <= 2 * std::max(1, nsm / cs);
+    if (const char* e = std::getenv("TT_WIDE")) wide = e[0] == '1';
+  }
+  if (wide)
+    cuda_check(launch_leaf_wide(prm, ex.d_desc.as<LeafDesc>(), n, cs, ex.stream), "leaf_wide_kernel launch");
+  else
+    cuda_check(launch_leaf(prm, ex.d_desc.as<LeafDesc>(), n, ex.stream), "leaf_als_kernel launch");
   std::vector<int32_t> hs(size_t(n) * kStatusInts);
   std::vector<double> ho(size_t(n) * prm.max_iters);
   cuda_check(cudaMemcpyAsync(hs.data(), ex.d_status.p, hs.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, ex.stream),
@@ -570,6 +599,16 @@ struct tt_tree {
   DevBuf tailq;  // tail-part scratch for queries
   double timing[3] = {0, 0, 0};
   mutable std::mutex qmu;
+  // Append journal: pre-call copies of the existing nodes an append modifies
+  // (at most the root-to-leaf paths), so a failed append can be rolled back.
+  Index journal_n0 = -1;
+  std::vector<HostNode> journal;
+  void journal_save(Index id) {
+    if (journal_n0 < 0 || id > journal_n0) return;
+    for (const HostNode& v : journal)
+      if (v.id == id) return;
+    journal.push_back(node(id));
+  }
 
   HostNode& node(Index id) { return nodes[static_cast<size_t>(id - 1)]; }
   const HostNode& node(Index id) const {
@@ -615,6 +654,7 @@ struct PendingWork {
 };
 
 void insert_leaf(tt_tree& t, Index id, Index leaf_idx, PendingWork& w) {
+  t.journal_save(id);
   ++t.last_touches;
   const Index b = t.node(id).begin / t.B, e = t.node(id).end / t.B;
   if (b == leaf_idx && e == leaf_idx + 1) {
@@ -943,20 +983,49 @@ tt_status tt_append(tt_tree* t, const double* slices, int64_t n, tt_mem where) {
       }
       (void)consumed;
     }
-    // Bookkeeping, one slice at a time (reference append semantics).
+    // Bookkeeping, one slice at a time (reference append semantics). A failed
+    // append leaves the tree unchanged (sst.cpp:95-97): the scalars, the node
+    // table and the arena are restored from a snapshot if anything below throws.
+    struct Snapshot {
+      Index nodes, root, timespan, leaves, stitch_count, last_touches;
+      std::vector<Index> last_redec;
+      Arena::Mark arena;
+    };
+    const Snapshot snap{static_cast<Index>(t->nodes.size()), t->root, t->timespan, t->leaves, t->stitch_count,
+                        t->last_touches, t->last_redec, t->arena ? t->arena->mark() : Arena::Mark{0, nullptr, 0}};
+    t->journal.clear();
+    t->journal_n0 = snap.nodes;
     PendingWork w;
     std::vector<Index> all_redec;
-    for (Index i = 0; i < n; ++i) {
-      ++t->timespan;
-      if (t->timespan - t->leaves * B == B) {
-        add_leaf(*t, w);
-        all_redec.insert(all_redec.end(), t->last_redec.begin(), t->last_redec.end());
-      } else {
-        t->last_touches = 0;
-        t->last_redec.clear();
+    try {
+      for (Index i = 0; i < n; ++i) {
+        ++t->timespan;
+        if (t->timespan - t->leaves * B == B) {
+          add_leaf(*t, w);
+          all_redec.insert(all_redec.end(), t->last_redec.begin(), t->last_redec.end());
+        } else {
+          t->last_touches = 0;
+          t->last_redec.clear();
+        }
       }
+      execute(*t, w, leaf_x);
+    } catch (...) {
+      if (!t->structure_only) cudaStreamSynchronize(t->ex->stream);  // no kernel still writes a dropped slot
+      t->nodes.resize(static_cast<size_t>(snap.nodes));
+      for (const HostNode& v : t->journal) t->node(v.id) = v;
+      t->root = snap.root;
+      t->timespan = snap.timespan;
+      t->leaves = snap.leaves;
+      t->stitch_count = snap.stitch_count;
+      t->last_touches = snap.last_touches;
+      t->last_redec = snap.last_redec;
+      if (t->arena) t->arena->release(snap.arena);
+      t->journal.clear();
+      t->journal_n0 = -1;
+      throw;
     }
-    execute(*t, w, leaf_x);
+    t->journal.clear();
+    t->journal_n0 = -1;
     if (!t->structure_only) {
       // New tail = slices past the last full block (after the leaf kernels read the old tail).
       const Index tail1 = t->timespan - t->leaves * B;
@@ -1373,14 +1442,34 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
         }
       } else {
         if (where == TT_MEM_HOST) t->qout.ensure(out_need * sizeof(double));
+        double* dscr = nullptr;  // device scratch for outputs the caller did not request (null pointers)
+        if (where == TT_MEM_DEVICE) {
+          size_t extra = 0;
+          for (int64_t q = q0; q < q1; ++q) {
+            const Index L = descs[q - q0].L;
+            if (!outs[q].core) extra += static_cast<size_t>(prod_range(t->cfg.ranks, 0, p)) + 32;
+            for (int m = 0; m < p; ++m)
+              if (!outs[q].factors[m]) extra += static_cast<size_t>((m == 0 ? L : t->d[m]) * t->clamped(m, L)) + 32;
+          }
+          if (extra) {
+            t->qscratch.ensure(extra * sizeof(double));
+            dscr = t->qscratch.as<double>();
+          }
+        }
         for (int64_t q = q0; q < q1; ++q) {
           StitchDesc& dsc = descs[q - q0];
           const Index L = dsc.L;
           Index rc[kMaxP];
           for (int m = 0; m < p; ++m) rc[m] = t->clamped(m, L);
           if (where == TT_MEM_DEVICE) {
-            for (int m = 0; m < p; ++m) dsc.out_f[m] = outs[q].factors[m];
-            dsc.out_core = outs[q].core;
+            auto scratch = [&dscr](Index nd) {
+              double* r = dscr;
+              dscr += nd + 32;
+              return r;
+            };
+            for (int m = 0; m < p; ++m)
+              dsc.out_f[m] = outs[q].factors[m] ? outs[q].factors[m] : scratch((m == 0 ? L : t->d[m]) * rc[m]);
+            dsc.out_core = outs[q].core ? outs[q].core : scratch(prod_range(t->cfg.ranks, 0, p));
           } else {
             double* cur = t->qout.as<double>() + out_off[q - q0];
             auto take = [&cur](Index nd) {
@@ -1556,6 +1645,7 @@ namespace {
 struct StandaloneCtx {
   std::unique_ptr<Exec> ex;
   int device = -1;
+  std::mutex op;  // one standalone operation at a time per device context (shared Exec buffers and stream)
 };
 StandaloneCtx& standalone(int device) {
   static std::mutex mu;
@@ -1600,6 +1690,7 @@ tt_status tt_tucker_als(const double* x, int32_t p, const int64_t* dims, const i
       if (ranks[m] > 32) fail(TT_EINVAL, "tucker_als: ranks above 32 are not supported by this build");
     }
     StandaloneCtx& c = standalone(device);
+    std::lock_guard<std::mutex> op_lock(c.op);
     Exec& ex = *c.ex;
     DeviceGuard g(device);
     Index d[kMaxP], rq[kMaxP], rc[kMaxP];
@@ -1672,6 +1763,7 @@ tt_status tt_brute_force_batch(const double* series, tt_mem where, int32_t p, co
     }
     if (n == 0) return;
     StandaloneCtx& c = standalone(device);
+    std::lock_guard<std::mutex> op_lock(c.op);
     Exec& ex = *c.ex;
     DeviceGuard g(device);
     Index d[kMaxP], rq[kMaxP];
@@ -1765,6 +1857,7 @@ tt_status tt_stitch(int32_t nparts, int32_t p, const int64_t* part_dims, const i
     for (int i = 0; i < nparts * p; ++i)
       if (part_ranks[i] > 32) fail(TT_EINVAL, "stitch: part ranks above 32 are not supported by this build");
     StandaloneCtx& c = standalone(device);
+    std::lock_guard<std::mutex> op_lock(c.op);
     Exec& ex = *c.ex;
     DeviceGuard g(device);
     Index d[kMaxP], rq[kMaxP], rc[kMaxP];
@@ -1868,6 +1961,7 @@ tt_status tt_partial_hit(int32_t p, const int64_t* dims, const int64_t* ranks, c
     Index rest = 1;
     for (int m = 1; m < p; ++m) rest *= ranks[m];
     StandaloneCtx& c = standalone(device);
+    std::lock_guard<std::mutex> op_lock(c.op);
     Exec& ex = *c.ex;
     DeviceGuard g(device);
     DevBuf bv, bc, bw, bq, br, bo, bt;

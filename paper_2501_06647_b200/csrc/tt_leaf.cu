@@ -151,11 +151,8 @@ __global__ void __launch_bounds__(kThreads, 2) leaf_als_kernel(Params prm, const
 
 cudaError_t launch_leaf(const Params& prm, const LeafDesc* d_descs, int n, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(leaf_als_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kLeafDynSmem));
-    attr = true;
-  }
+  const cudaError_t ae = ensure_dyn_smem(reinterpret_cast<const void*>(leaf_als_kernel), 0, kLeafDynSmem);
+  if (ae != cudaSuccess) return ae;
   leaf_als_kernel<<<n, kThreads, kLeafDynSmem, st>>>(prm, d_descs);
   g_launches.fetch_add(1);
   return cudaGetLastError();

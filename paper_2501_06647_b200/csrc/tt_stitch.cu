@@ -3,6 +3,8 @@
 // r-sized coordinates: the L-row temporal unfolding is never formed
 // (SURVEY.md A.2); partial hits enter through the Gram S = Vsub^T Vsub of
 // their kept temporal rows instead of a QR.
+#include <mutex>
+
 #include "tt_dev.cuh"
 
 namespace ttb {
@@ -1056,6 +1058,20 @@ __global__ void __launch_bounds__(256) copy_segments_kernel(const CopySeg* __res
 
 std::atomic<int64_t> g_launches{0};
 
+cudaError_t ensure_dyn_smem(const void* fn, int slot, size_t bytes) {
+  static std::mutex mu;
+  static uint64_t done[8] = {};  // bit d of done[slot]: set on device d
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  if (done[slot] & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+  if (e == cudaSuccess) done[slot] |= bit;
+  return e;
+}
+
 // ---------------------------------------------------------------------------
 // partial_hit_factors (stitch.cpp:36-47) for the standalone API: thin
 // Householder QR of the kept temporal rows V0[b:e, :] (len x n, n <= 32), in
@@ -1181,11 +1197,8 @@ cudaError_t launch_copy_segments(const CopySeg* d_segs, int n, cudaStream_t st) 
 cudaError_t launch_stitch(const Params& prm, const StitchDesc* d_descs, const StitchPart* d_parts, int n,
                           cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(stitch_als_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDynSmem));
-    attr = true;
-  }
+  const cudaError_t ae = ensure_dyn_smem(reinterpret_cast<const void*>(stitch_als_kernel), 1, kDynSmem);
+  if (ae != cudaSuccess) return ae;
   stitch_als_kernel<<<n, kStitchThreads, kDynSmem, st>>>(prm, d_descs, d_parts);
   g_launches.fetch_add(1);
   return cudaGetLastError();
