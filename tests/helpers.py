@@ -79,9 +79,9 @@ def max_sin_angle(a: np.ndarray, b: np.ndarray) -> float:
         return 0.0
     qa, _ = np.linalg.qr(a)
     qb, _ = np.linalg.qr(b)
-    s = np.linalg.svd(qa.T @ qb, compute_uv=False)
-    c = float(np.clip(np.min(s), 0.0, 1.0))
-    return math.sqrt(max(0.0, 1.0 - c * c))
+    # ||(I - Qa Qa^T) Qb||_2 = sin of the largest angle, accurate to rounding
+    # (the 1 - cos^2 route bottoms out near 1e-8)
+    return float(np.linalg.norm(qb - qa @ (qa.T @ qb), 2))
 
 
 def admissible_pieces(nodes, ts, te, theta, leaf_block=1):
