@@ -1,21 +1,28 @@
 """Benchmark of the stream-segment-tree hot path on B200 (BASELINE.json metric:
 range-Tucker queries/sec & appended slices/sec, with roofline fractions).
 
-Workload (config.workload, default "c2" = BASELINE.json configs[1]): series
-(T=32768, 376, 6) fp64, ranks (10,10,4), leaf block 128, 1000 range queries of
-length U[64, T]. One step = build the tree from scratch (burst append of all T
-slices: 256 batched leaf ALS + 255 stitches, level-synchronous) and answer the
-1000-query batch. Series and outputs are HBM-resident for `value`; `e2e` runs
-the same step through the public API with pinned host buffers (H2D of the
-slices and D2H of every query result inside the timed region).
+Default workload = BASELINE.json configs[2] (C3), the largest configuration
+that fits one GPU (5.77 GB series), in its BASELINE form: series
+(T=16384, 500, 88) fp64 with Student-t(df=3) entries on a rank-(10,10,10)
+backbone, leaf block 64; the tree is built from the first 12288 slices
+(setup, reported as "build"), then slices are appended ONE AT A TIME with one
+range query over the current [0, T) after every 16 appends.
+One step = one leaf block of the stream: 64 single-slice appends + 4 queries
+(the append that completes the block runs the leaf ALS and its stitch chain).
+`value` = queries/s of that interleaved stream (slices, resident in HBM, are
+appended from device memory; query outputs land in device buffers);
+`append.value` = streamed slices/s of the same run; `e2e` = the same stream
+through the public C ABI from pinned HOST slices with HOST query outputs.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl engine|reference]
+                  [--config c1|c2|c3|c4] [--form stream|burst]
 
-Multi-GPU (torchrun): every rank builds its own replica and answers its own
-query shard (independent seeds) — the path shards with no data-path
-collective ("scaling": "weak"); times are max over ranks via NCCL all-reduce.
---impl reference times the CPU restatement of the reference (oracle/, the
-reference itself cannot be built here) on the host cores, rank 0 only.
+--form burst (default for C1/C2/C4) is the round-1 step: build the whole tree
+from HBM in one burst append, then one batched query launch.
+Multi-GPU (torchrun): every rank runs an independent replica on its own seeded
+series (no data-path collective, "scaling": "weak"); times are max over ranks.
+--impl reference times the CPU restatement of the reference (oracle/, pinned to
+the reference's own sources by tests/test_ref_pin.py) on the host cores.
 """
 from __future__ import annotations
 
@@ -147,7 +154,7 @@ def run_engine(args, rank, world, local_rank):
     w = synth.CONFIGS[args.config]
     T = w.shape[0]
     nq = args.queries or w.n_queries
-    x = synth.generate(w, seed=0)
+    x = synth.generate(w, seed=rank)  # independent replica per rank (weak scaling counts distinct work)
     ranges = synth.ranges(w, T, nq, seed=1 + rank)
     L = eng.lib()
     xd = torch.from_numpy(x).to(dev)
@@ -375,13 +382,370 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# Streaming form (BASELINE C3): single-slice appends with interleaved queries.
+def stream_layout(w, steps_total):
+    """(T0, block, per_query, T_series): the series is the config's T unless
+    more steps than its 4096 streamed slices are asked for."""
+    B = w.leaf_block
+    T0 = w.build_T
+    need = T0 + B * steps_total
+    return T0, B, 16, max(w.shape[0], need)
+
+
+def stream_alg_bytes(w, T_hits, hits, L):
+    """SURVEY §8(d)(c) algorithmic bytes of one query given its hit list."""
+    nt = sum(d * r for d, r in zip(w.shape[1:], w.ranks[1:]))
+    pr = int(np.prod(w.ranks))
+    rows = sum((h.end - h.begin) * w.ranks[0] for h in hits)
+    return 8 * (rows + len(hits) * (nt + pr) + L * min(w.ranks[0], L) + nt + pr)
+
+
+def run_engine_stream(args, rank, world, local_rank):
+    import torch
+
+    import paper_2501_06647_b200 as eng
+    from paper_2501_06647_b200 import synth
+    from paper_2501_06647_b200.tucktree import TTQueryOut, TTRange, dptr
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    w = synth.CONFIGS[args.config]
+    K, Wm = args.steps, args.warmup
+    T0, B, every, Tser = stream_layout(w, K + Wm)
+    # the series is generated on the device (the 5.8 GB numpy path takes ~1 min);
+    # only the streamed slices are staged in pinned host memory for e2e
+    xd = synth.generate_torch(w, seed=rank, T=Tser, device=dev)  # independent replica per rank
+    ss = int(np.prod(w.shape[1:]))
+    p = len(w.ranks)
+    L = eng.lib()
+    xh = xd[T0:].cpu().pin_memory()
+    r0 = w.ranks[0]
+    rc = [min(r, d) for r, d in zip(w.ranks[1:], w.shape[1:])]
+    out_n = int(np.prod(w.ranks)) + Tser * r0 + sum(d * r for d, r in zip(w.shape[1:], rc))
+    dq = torch.empty(out_n, dtype=torch.float64, device=dev)
+    hq = torch.empty(out_n, dtype=torch.float64).pin_memory()
+
+    def outs_for(buf, Tn):
+        o = TTQueryOut()
+        base = buf.data_ptr()
+        o.core = C.cast(C.c_void_p(base), dptr)
+        off = int(np.prod(w.ranks))
+        o.factors[0] = C.cast(C.c_void_p(base + 8 * off), dptr)
+        off += Tn * r0
+        for m in range(1, p):
+            o.factors[m] = C.cast(C.c_void_p(base + 8 * off), dptr)
+            off += w.shape[m] * rc[m - 1]
+        return o, 8 * (int(np.prod(w.ranks)) + Tn * min(r0, Tn) + sum(d * r for d, r in zip(w.shape[1:], rc)))
+
+    mk = lambda: eng.StreamSegmentTree(w.shape[1:], w.ranks, leaf_block=B, device=local_rank)
+    tree, tree_e = mk(), mk()
+    # ---- setup: burst build of the first T0 slices (timed separately as "build")
+    torch.cuda.synchronize()
+    b0 = time.perf_counter()
+    tree.append_device(xd.data_ptr(), T0)
+    build_s = time.perf_counter() - b0
+    build_ms = tree.last_timing_ms()
+    tree_e.append_device(xd.data_ptr(), T0)
+    torch.cuda.synchronize()
+    acc = {"leaf": 0.0, "stitch": 0.0, "tail": 0.0, "qstitch": 0.0}
+    lat_app, lat_leafapp, lat_q = [], [], []
+    alg = {"leaf": 0, "stitch": 0}
+    nleaf = [0]
+
+    def stream_step(tr, c, where, buf, record):
+        """One leaf block: B single-slice appends, a [0, T) query every `every`."""
+        Tcur = tr.timespan()
+        for j in range(B):
+            t = Tcur + j
+            if where == 1:
+                src = C.cast(C.c_void_p(xd.data_ptr() + 8 * t * ss), dptr)
+            else:
+                src = C.cast(C.c_void_p(xh.data_ptr() + 8 * (t - T0) * ss), dptr)
+            a0 = time.perf_counter()
+            eng.tucktree._check(L.tt_append(tr._h, src, 1, where))
+            da = time.perf_counter() - a0
+            if record:
+                ms = tr.last_timing_ms()
+                done_leaf = (t + 1) % B == 0
+                lat_app.append(da)
+                if done_leaf:
+                    lat_leafapp.append(da)
+                    acc["leaf"] += ms[0]
+                    acc["stitch"] += ms[1]
+                    nleaf[0] += 1
+                    alg["leaf"] += 8 * B * ss
+                    # stitch chain: parent lengths 2B, 4B, ... while the node completes
+                    lv, li = 1, (t + 1) // B
+                    while li % (1 << lv) == 0:
+                        Lp = B << lv
+                        # two children's rows + factors + cores read, the parent's L x r0 written
+                        nt_pr = sum(d * r for d, r in zip(w.shape[1:], rc)) + int(np.prod(w.ranks))
+                        alg["stitch"] += 8 * (Lp * r0 + 2 * nt_pr + Lp * r0)
+                        lv += 1
+            if (j + 1) % every == 0:
+                Tn = t + 1
+                rr = TTRange()
+                rr.ts, rr.te = 0, Tn
+                o, ob = outs_for(buf, Tn)
+                q0 = time.perf_counter()
+                eng.tucktree._check(L.tt_query_batch(tr._h, C.byref(rr), 1, float("nan"), C.byref(o), where))
+                dq_ = time.perf_counter() - q0
+                if record:
+                    ms = tr.last_timing_ms()
+                    lat_q.append(dq_)
+                    acc["tail"] += ms[0]
+                    acc["qstitch"] += ms[1]
+                    hits = tr.recall(0, Tn)
+                    alg["stitch"] += stream_alg_bytes(w, Tn, [h for h in hits if h.flag != 2], Tn)
+                    alg["leaf"] += 8 * sum(h.end - h.begin for h in hits if h.flag == 2) * ss
+
+    # ---------------- device-resident (value) ----------------
+    for c in range(Wm):
+        stream_step(tree, c, 1, dq, False)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = eng.kernel_launches()
+    stats0 = eng.solver_stats()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        ev0.record()
+        for c in range(K):
+            stream_step(tree, Wm + c, 1, dq, True)
+        ev1.record()
+        torch.cuda.synchronize()
+    span_ms = ev0.elapsed_time(ev1)
+    launches = eng.kernel_launches() - launches0
+    stats1 = eng.solver_stats()
+    solver = {k: (stats1[k] - stats0[k]) / K for k in ("problems", "als_sweeps", "eig_calls", "jacobi_sweeps",
+                                                       "subspace_ok", "subspace_fallback", "subspace_iters")}
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    # ---------------- end to end: pinned host slices in, host outputs out ----------------
+    for c in range(Wm):
+        stream_step(tree_e, c, 0, hq, False)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for c in range(K):
+        stream_step(tree_e, Wm + c, 0, hq, False)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    vals = torch.tensor([span_ms, e2e_ms, acc["leaf"], acc["stitch"], acc["tail"], acc["qstitch"]],
+                        dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    span_ms, e2e_ms, t_leaf, t_stitch, t_tail, t_qstitch = [float(v) for v in vals.tolist()]
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    nq = K * (B // every)
+    qps = world * nq / (span_ms / 1e3)
+    sps = world * K * B / (span_ms / 1e3)
+    peak, peak_kind = _peaks()
+    t_leafk = t_leaf + t_tail
+    t_stk = t_stitch + t_qstitch
+    traffic = load_traffic(w.name + "_stream")
+    if t_stk >= t_leafk:
+        gbs = alg["stitch"] / (t_stk / 1e3) / 1e9
+        roof = {"kernel": "stitch_als_kernel (append stitch chains + [0,T) query stitches)", "bound": "hbm",
+                "achieved": round(gbs, 3), "peak": peak, "unit": "GB/s", "frac": round(gbs / peak, 6),
+                "traffic": traffic.get("stitch"), "algorithmic_bytes_per_step": alg["stitch"] // K,
+                "peak_kind": peak_kind}
+    else:
+        gbs = alg["leaf"] / (t_leafk / 1e3) / 1e9
+        roof = {"kernel": "leaf_wide_kernel (streamed leaf blocks + query tails)", "bound": "hbm",
+                "achieved": round(gbs, 3), "peak": peak, "unit": "GB/s", "frac": round(gbs / peak, 6),
+                "traffic": traffic.get("leaf"), "algorithmic_bytes_per_step": alg["leaf"] // K,
+                "peak_kind": peak_kind}
+    la, ll, lq = (np.array(v) * 1e3 for v in (lat_app, lat_leafapp, lat_q))
+    q_out_bytes = sum(outs_for(dq, T0 + Wm * B + c * B + (j + 1) * every)[1] for c in range(K) for j in range(B // every))
+    build_gbs = 8 * T0 * ss / (build_ms[0] / 1e3) / 1e9 if build_ms[0] > 0 else None
+    line = {
+        "metric": "range_tucker_queries_per_s",
+        "value": round(qps, 3),
+        "unit": "queries/s",
+        "n_gpus": world,
+        "steps": K,
+        "warmup": Wm,
+        "ms_per_step": round(span_ms / K, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded; " + w.desc + ")",
+        "config": {"workload": w.name + "_stream", "shape": [Tser] + list(w.shape[1:]), "ranks": list(w.ranks),
+                   "leaf_block": B, "build_slices": T0, "slices_per_step": B, "queries_per_step": B // every,
+                   "query": "[0, T) over the current timespan after every 16th single-slice append",
+                   "l2": "inputs larger than L2 (the 5.8 GB series streams slice by slice; every leaf block and "
+                         "query tail is read from HBM the first time it is touched)",
+                   "step": "64 single-slice appends from HBM (one completes a leaf block: leaf ALS + stitch chain) "
+                           "+ 4 range queries [0, T)"},
+        "append": {"value": round(sps, 3), "unit": "slices/s", "latency_ms": {
+            "p50": round(float(np.median(la)), 4), "p99": round(float(np.percentile(la, 99)), 4),
+            "block_completing_p50": round(float(np.median(ll)), 4),
+            "block_completing_p99": round(float(np.percentile(ll, 99)), 4),
+            "block_completing_max": round(float(ll.max()), 4)}},
+        "query_latency_ms": {"p50": round(float(np.median(lq)), 4), "p99": round(float(np.percentile(lq, 99)), 4),
+                             "max": round(float(lq.max()), 4)},
+        "phases_ms_per_step": {"append_leaf_als": round(t_leaf / K, 4), "append_stitch_chain": round(t_stitch / K, 4),
+                               "query_tail_als": round(t_tail / K, 4), "query_stitch": round(t_qstitch / K, 4),
+                               "host_and_sync": round((span_ms - t_leaf - t_stitch - t_tail - t_qstitch) / K, 4)},
+        "build": {"slices": T0, "slices_per_s": round(T0 / build_s, 1), "device_ms": round(float(build_ms[2]), 3),
+                  "leaf_phase_ms": round(float(build_ms[0]), 3), "stitch_phase_ms": round(float(build_ms[1]), 3),
+                  "leaf_phase_gbs": round(build_gbs, 2) if build_gbs else None,
+                  "leaf_phase_frac": round(build_gbs / peak, 5) if build_gbs else None},
+        "e2e": {"value": round(world * nq / (e2e_ms / 1e3), 3), "unit": "queries/s",
+                "h2d_bytes_per_step": int(B * ss * 8), "d2h_bytes_per_step": int(q_out_bytes // K),
+                "append_slices_per_s": round(world * K * B / (e2e_ms / 1e3), 3)},
+        "roofline": roof,
+        "gpu_launches": int(launches),
+        "solver_per_step": solver,
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_stream_sample(w, xh.numpy(), T0, args)
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def load_traffic(key):
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        t = json.load(open(prof))
+        v = t.get(key)
+        return v if isinstance(v, dict) else {}
+    except Exception:
+        return {}
+
+
+def _synthetic_node(rng, L, w, ref):
+    """A stored-node-shaped part (L-row temporal factor, the config's non-temporal
+    factors, full core) for timing the CPU stitch: cost depends on shapes only."""
+    from oracle import oracle as O
+
+    q, _ = np.linalg.qr(rng.standard_normal((L, min(w.ranks[0], L))))
+    core = rng.standard_normal([q.shape[1]] + [ref.rank(m) for m in range(1, len(w.ranks))])
+    return O.Factors(core, [q] + [ref.factors[m] for m in range(1, len(w.ranks))])
+
+
+def cpu_stream_cycle(w, xs, T0, c, threads, cache):
+    """CPU time (s) of streaming cycle c on the oracle: the leaf ALS of the
+    completed block, its stitch chain (two-part stitches of lengths 2B, 4B, ...)
+    and the 4 [0, T) queries (tail ALS + stitch of the entire hits + tail)."""
+    from oracle import oracle as O
+
+    O.set_threads(threads)
+    B = w.leaf_block
+    rng = np.random.default_rng(c)
+    t_start = time.perf_counter()
+    li = T0 // B + c  # index of the leaf this cycle completes
+    leaf = O.tucker_als(xs[li * B - T0:(li + 1) * B - T0], w.ranks)  # xs starts at slice T0
+    cache.setdefault("leaf", leaf)
+    lv = 1
+    while (li + 1) % (1 << lv) == 0:
+        Lp = B << lv
+        parts = [_synthetic_node(rng, Lp // 2, w, leaf), _synthetic_node(rng, Lp // 2, w, leaf)]
+        O.stitch(parts, w.ranks)
+        lv += 1
+    for j in range(B // 16):
+        tail = 16 * (j + 1) if j + 1 < B // 16 else 0
+        nb = li + (1 if tail == 0 else 0)  # complete leaves at this query
+        parts = []
+        if tail:
+            Ts = (li) * B
+            parts_tail = O.tucker_als(xs[Ts - T0:Ts - T0 + tail], w.ranks)
+        else:
+            parts_tail = None
+        # entire hits of [0, nb*B): the binary decomposition of nb
+        bit = 1 << max(nb.bit_length() - 1, 0)
+        while bit:
+            if nb & bit:
+                parts.append(_synthetic_node(rng, bit * B, w, leaf))
+            bit >>= 1
+        if parts_tail is not None:
+            parts.append(parts_tail)
+        O.stitch(parts, w.ranks)
+    return time.perf_counter() - t_start
+
+
+def cpu_stream_sample(w, xs, T0, args):
+    """cpu_baseline for the streaming form: the oracle on sampled cycles (single
+    thread, reference-faithful) — leaf ALS, stitch chain and 4 queries each."""
+    cache = {}
+    picks = [0, 15, 31, 63][: max(1, args.cpu_cycles)]
+    ts = [cpu_stream_cycle(w, xs, T0, c, 1, cache) for c in picks if (c + 1) * w.leaf_block <= xs.shape[0]]
+    per = sum(ts) / len(ts)
+    return {"value": round((w.leaf_block // 16) / per, 4), "unit": "queries/s", "cores": 1, "kind": "port",
+            "sample": f"oracle (restated reference, 1 thread) on {len(ts)} sampled stream cycles {picks[:len(ts)]}: "
+                      f"leaf ALS of the completed 64-slice block + its stitch chain + 4 [0, T) queries (tail ALS + "
+                      f"stitch of the entire hits; hit nodes carry stored-node shapes), {per:.2f} s per cycle",
+            "append_slices_per_s": round(w.leaf_block / per, 3)}
+
+
+def run_reference_stream(args, rank, world):
+    """--impl reference for the streaming form: each step = one stream cycle on
+    the oracle with all host cores given to its BLAS."""
+    if rank != 0:
+        return
+    from paper_2501_06647_b200 import synth
+
+    w = synth.CONFIGS[args.config]
+    K, Wm = args.steps, args.warmup
+    T0, B, every, Tser = stream_layout(w, K + Wm)
+    # same seeded series as the engine arm (generated with torch, on the GPU when
+    # present — input synthesis only, outside every timed region); the CPU
+    # works on the streamed slices
+    import torch
+
+    gdev = "cuda" if torch.cuda.is_available() else "cpu"
+    xs = synth.generate_torch(w, seed=0, T=Tser, device=gdev)[T0:].cpu().numpy()
+    cores = os.cpu_count() or 1
+    cache = {}
+    ncyc = (Tser - T0) // B
+    for c in range(Wm):
+        cpu_stream_cycle(w, xs, T0, c % ncyc, cores, cache)
+    tot = 0.0
+    for i in range(K):
+        tot += cpu_stream_cycle(w, xs, T0, (Wm + i) % ncyc, cores, cache)
+    qps = K * (B // every) / tot
+    line = {
+        "metric": "range_tucker_queries_per_s", "value": round(qps, 4), "unit": "queries/s", "n_gpus": world,
+        "steps": K, "warmup": Wm, "ms_per_step": round(1e3 * tot / K, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; " + w.desc + ")",
+        "config": {"workload": w.name + "_stream", "shape": [Tser] + list(w.shape[1:]), "ranks": list(w.ranks),
+                   "leaf_block": B, "build_slices": T0, "slices_per_step": B, "queries_per_step": B // every},
+        "impl": "reference",
+        "append": {"value": round(K * B / tot, 3), "unit": "slices/s"},
+        "cpu_baseline": {"value": round(qps, 4), "unit": "queries/s", "cores": cores, "kind": "port",
+                         "sample": f"per step one stream cycle on the oracle (restated reference): leaf ALS of the "
+                                   f"completed block, its stitch chain, 4 [0, T) queries; BLAS on {cores} threads"},
+        "e2e": {"value": round(qps, 4), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--form", default="", choices=["", "stream", "burst"])
+    ap.add_argument("--cpu-cycles", type=int, default=2)
     ap.add_argument("--queries", type=int, default=0)
     ap.add_argument("--cpu-queries", type=int, default=64)
     ap.add_argument("--ref-queries", type=int, default=32)
@@ -391,10 +755,13 @@ def main():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    from paper_2501_06647_b200 import synth
+
+    form = args.form or ("stream" if synth.CONFIGS[args.config].build_T else "burst")
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        (run_reference_stream if form == "stream" else run_reference)(args, rank, world)
     else:
-        run_engine(args, rank, world, local_rank)
+        (run_engine_stream if form == "stream" else run_engine)(args, rank, world, local_rank)
 
 
 if __name__ == "__main__":

@@ -1,0 +1,34 @@
+"""compute-sanitizer memcheck and racecheck over tools/sanitize_smoke.py, which
+launches every engine kernel (batched and cluster leaf ALS, stitch levels,
+query batch, partial hit, brute force) on small shapes (race
+detection / sanitizers). The run fails on any reported error."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+def _run(tool, timeout):
+    if not os.path.exists(SAN):
+        pytest.skip("compute-sanitizer not installed")
+    cmd = [SAN, "--tool", tool, "--error-exitcode", "9", "--print-limit", "20", sys.executable,
+           os.path.join(ROOT, "tools", "sanitize_smoke.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and "sanitize smoke ok" in out, out[-4000:]
+    assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
+
+
+@pytest.mark.gpu
+def test_memcheck_clean():
+    _run("memcheck", 900)
+
+
+@pytest.mark.gpu
+def test_racecheck_clean():
+    _run("racecheck", 1500)
