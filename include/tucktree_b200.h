@@ -16,6 +16,7 @@
  *      TT_EINVAL  <- std::invalid_argument  (bad shapes, ranges, theta, config)
  *      TT_ELOGIC  <- std::logic_error       (structural impossibilities)
  *      TT_EIO     <- std::runtime_error     (I/O)
+ *      TT_ERANGE  <- std::out_of_range      (unknown node id, sst.cpp:68)
  *    plus TT_ECUDA / TT_ENOMEM for device failures. tt_last_error() returns the
  *    thread-local message of the last failure.
  *  - A failed append leaves the tree unchanged (sst.cpp:95-97).
@@ -42,7 +43,8 @@ typedef enum tt_status {
   TT_EIO = 3,
   TT_ECUDA = 4,
   TT_ENCCL = 5,
-  TT_ENOMEM = 6
+  TT_ENOMEM = 6,
+  TT_ERANGE = 7
 } tt_status;
 
 /* Where a caller buffer lives. */
@@ -97,8 +99,13 @@ typedef struct tt_range {
  *   core:        prod_n r_n doubles (row-major, actual ranks)
  *   factors[0]:  L x r_0  (column-major, ld = L = te - ts)
  *   factors[m]:  D_m x r_m (column-major, ld = D_m)
+ * A null core/factor pointer means "not requested" (the engine uses scratch).
  * Outputs written by the engine: ranks (actual column counts), sweeps,
- * converged, objective (final squared residual), nhits. */
+ * converged, objective (final squared residual), nhits, and — when trace is
+ * non-null — the per-sweep squared residuals (AlsTrace::objective,
+ * tucker.hpp:25-28) into trace[0 .. min(sweeps, trace_cap)), and — when hits
+ * is non-null — the hit set the query used into hits[0 .. min(nhits,
+ * hits_cap)) (trace and hits: host memory). */
 typedef struct tt_query_out {
   double* core;
   double* factors[TT_MAX_ORDER];
@@ -107,6 +114,10 @@ typedef struct tt_query_out {
   int32_t converged;
   double objective;
   int32_t nhits;
+  int32_t trace_cap;  /* capacity of trace (doubles); 0: no trace */
+  double* trace;      /* host buffer for the per-sweep objective, or NULL */
+  tt_hit* hits;       /* host buffer for the hit set (QueryResult::hits), or NULL */
+  int32_t hits_cap;   /* capacity of hits */
   int32_t pad;
 } tt_query_out;
 
@@ -133,6 +144,16 @@ tt_status tt_append(tt_tree* tree, const double* slices, int64_t n, tt_mem where
  * API (equivalent to constructing a new StreamSegmentTree).               */
 tt_status tt_tree_clear(tt_tree* tree);
 
+/* StreamSegmentTree::from_parts (sst.hpp:58-62): rebuilds a tree from node
+ * records (ids 1..n in order; semantic invariants are checked by tt_validate,
+ * not here) and, for nodes with has_decomposition, their payloads:
+ * cores[i] (row-major, nodes[i].ranks) and factors[i*order + m] (column-major;
+ * factor 0 is length x r_0, factor m is D_m x r_m), host memory. The
+ * leaf block is cfg->leaf_block (1 = the reference tree); timespan must be a
+ * multiple of it (the raw tail of a B > 1 tree is not part of the parts).   */
+tt_status tt_tree_from_parts(const tt_config* cfg, const tt_node_info* nodes, int64_t n,
+                             const double* const* cores, const double* const* factors, int64_t root,
+                             int64_t timespan, int64_t stitch_count, tt_tree** out);
 /* timespan / height / stitch_count / last_append_node_touches / node_count /
  * root / leaves                                            sst.hpp:69-91 */
 enum {
@@ -239,6 +260,10 @@ int32_t tt_factors_converged(const tt_factors* f);
 const double* tt_factors_objective(const tt_factors* f); /* per-sweep squared residual (AlsTrace) */
 void tt_factors_free(tt_factors* f);
 
+/* Fault injection (tests): the next n tt_append calls that
+ * complete a leaf block fail with TT_ECUDA after their leaf kernels ran, and
+ * must leave the tree unchanged (sst.cpp:95-97).                           */
+void tt_debug_fail_appends(int32_t n);
 /* Number of the engine's own kernels launched since process start (the bench
  * reports the delta over its timed region).                               */
 int64_t tt_kernel_launches(void);

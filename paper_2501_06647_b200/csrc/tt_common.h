@@ -125,7 +125,7 @@ constexpr int kStatusInts = 4 + kMaxP + 17;  // ..., eig calls, Jacobi sweeps, k
 constexpr int64_t kMisc = 2048;
 
 struct LeafWs {
-  int64_t W, B1, B2, G, V, SI, misc, xch, total, gram_n;
+  int64_t W, B1, B2, G, V, SI, misc, xch, gpart, total, gram_n;
 };
 // Cross-CTA exchange slots of the cluster leaf kernel (per-CTA partial sums, stop flag).
 constexpr int64_t kXch = 64;
@@ -136,7 +136,8 @@ TT_HD int64_t si_size(int64_t max_rows, int64_t max_cols, int64_t kmax) {
   return 2 * max_rows * kmax + max_cols * kmax + 8 * kmax * kmax + max_cols + 64;
 }
 
-TT_HD LeafWs leaf_ws_layout(int p, int64_t len, const int64_t* d, const int64_t* req) {
+// cs > 0: the cluster kernel's per-CTA partial Gram slots (cs x gram_n^2).
+TT_HD LeafWs leaf_ws_layout(int p, int64_t len, const int64_t* d, const int64_t* req, int64_t cs = 0) {
   int64_t dd[kMaxP], rc[kMaxP];
   dd[0] = len;
   for (int m = 1; m < p; ++m) dd[m] = d[m];
@@ -162,7 +163,8 @@ TT_HD LeafWs leaf_ws_layout(int p, int64_t len, const int64_t* d, const int64_t*
   w.SI = w.V + g * g;
   w.misc = w.SI + si_size(maxrows, g, kmax);
   w.xch = w.misc + kMisc + 4 * g;
-  w.total = w.xch + kXch;
+  w.gpart = w.xch + kXch;
+  w.total = w.gpart + cs * g * g;
   w.total = (w.total + 31) & ~int64_t(31);
   return w;
 }

@@ -20,6 +20,8 @@ constexpr int kStitchCtas = TT_STITCH_CTAS;  // resident stitch CTAs per SM (reg
 #define TT_STITCH_DYN_KB 56  // measured: 56 KB (more L1 at 2 CTAs/SM) beats 64 and 48 by 3%
 #endif
 constexpr size_t kDynSmem = kStitchCtas >= 3 ? size_t(55) * 1024 : size_t(TT_STITCH_DYN_KB) * 1024;
+// small stitch batches: one CTA per SM with most of the SM's shared memory
+constexpr size_t kDynSmemSolo = size_t(200) * 1024;
 
 __device__ __forceinline__ unsigned dyn_smem_doubles() {
   unsigned b;
@@ -558,13 +560,37 @@ __device__ __noinline__ double* sym_topk_si_k(const double* __restrict__ G, int 
                                               double* lam, int* order, double* dsm, BlockScratch& sc) {
   double* small = dsm + 768;  // CholeskyQR scratch (3 K^2); dsm[0, 768) is the Rayleigh-Ritz eigensolver's
   double* B = dsm + 1536;     // K x K
+  // With room, G (odd leading dimension: conflict-free row reads), U and W live
+  // in shared memory for the whole iteration: every product is then an SMEM
+  // stream instead of an L2-latency-bound dot product (the cluster leaf
+  // kernel's 176 KB and the stitch kernel's small-batch launches have room for
+  // n = 100).
+  const int ldg = n | 1;
+  const bool staged = 2048 + ldg * n + 2 * n * K <= sc.dsm_cap;
+  double* const Ug = U;
+  double* const Wg = W;
+  const double* Gp = G;
+  int ldp = n;
+  if (staged) {
+    double* Gs = dsm + 2048;
+    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+      const int i = idx % n, j = idx / n;
+      Gs[i + j * ldg] = G[idx];
+    }
+    U = Gs + ldg * n;
+    W = U + n * K;
+    for (int idx = threadIdx.x; idx < n * K; idx += blockDim.x) U[idx] = Ug[idx];
+    Gp = Gs;
+    ldp = ldg;
+    __syncthreads();
+  }
   if (!cholqr_pass_k<K>(U, n, small, sc) || !cholqr_pass_k<K>(U, n, small, sc)) return nullptr;
   bool conv = false;
   int it = 0;
   for (; it < kGramSiMaxIter; ++it) {
     for (int idx = threadIdx.x; idx < n * K; idx += blockDim.x) {
       const int i = idx % n, j = idx / n;
-      W[idx] = dot4(G + int64_t(i) * n, 1, U + int64_t(j) * n, 1, n);
+      W[idx] = dot4(Gp + int64_t(i) * ldp, 1, U + int64_t(j) * n, 1, n);
     }
     __syncthreads();
     gemm(K, K, n, U, n, 1, W, 1, n, B, 1, K, false, sc);  // B = U^T W
@@ -621,6 +647,11 @@ __device__ __noinline__ double* sym_topk_si_k(const double* __restrict__ G, int 
   }
   if (threadIdx.x < K) lam[threadIdx.x] = diag[order[threadIdx.x] * (K + 1)];
   __syncthreads();
+  if (staged) {  // hand the result back in the caller's global buffer
+    for (int idx = threadIdx.x; idx < n * K; idx += blockDim.x) Wg[idx] = W[idx];
+    __syncthreads();
+    return Wg;
+  }
   return W;
 }
 
@@ -648,12 +679,18 @@ constexpr int kGramTiledMinN = 24;
 // row-major (outer, rows, inner) tensor, through the Gram matrix of its
 // smaller side. U: rows x k (ld rows), sign-fixed. On entry U holds the
 // factor's current value (kprev columns), used as the iterations' warm start.
+// gram_ready: G already holds the Gram of the smaller side (the cluster
+// kernel forms it across its CTAs, tt_wide.cu); skip straight to the solver.
+__device__ __forceinline__ bool llsv_uses_subspace(int64_t rows, int64_t cols, int64_t k, int64_t kprev,
+                                                   const double* si, const BlockScratch& sc) {
+  return si != nullptr && kprev > 0 && rows > cols && cols >= 2 * k && cols * k <= kSiMaxYK && k <= kSiMaxK &&
+         si_base() + kSiMaxYK + 5 * k * k + 256 <= sc.dsm_cap;
+}
 static __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows, int64_t inner, int64_t k, double* U,
                             double* G, double* V, double* misc, double* dsm, BlockScratch& sc, int64_t kprev = 0,
-                            double* si = nullptr) {
+                            double* si = nullptr, bool gram_ready = false) {
   const int64_t cols = outer * inner;
-  if (si != nullptr && kprev > 0 && rows > cols && cols >= 2 * k && cols * k <= kSiMaxYK && k <= kSiMaxK &&
-      si_base() + kSiMaxYK + 5 * k * k + 256 <= sc.dsm_cap) {
+  if (!gram_ready && llsv_uses_subspace(rows, cols, k, kprev, si, sc)) {
     const long long t0 = tstart();
     const bool ok = llsv_subspace(P, outer, rows, inner, int(k), int(imin(kprev, k)), U, si, dsm, misc, sc);
     tstop(sc, kPhEig, t0);
@@ -674,7 +711,9 @@ static __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows,
     const int64_t o = c / inner, t = c - o * inner;
     return P[(o * rows + i) * inner + t];
   };
-  if (n >= kGramTiledMinN && n * 4 <= sc.dsm_cap) {
+  if (gram_ready) {
+    // formed by the caller
+  } else if (n >= kGramTiledMinN && n * 4 <= sc.dsm_cap) {
     if (wide)  // G = A A^T: x runs over the columns c (contiguous in t)
       gram_tiled(n, cols, [&](int64_t c, int a) { return unf(a, c); }, true, G, dsm, sc.dsm_cap);
     else  // G = A^T A: x runs over the rows i, a over the columns

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -22,6 +23,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/tucktree_b200.h"
@@ -47,8 +49,11 @@ using Index = int64_t;
 namespace {
 
 thread_local std::string g_err;
+std::atomic<uint64_t> g_stamp{0};
+std::atomic<int32_t> g_fail_appends{0};  // tt_debug_fail_appends
+uint64_t next_stamp() { return g_stamp.fetch_add(1) + 1; }
 // problems, ALS sweeps, eig calls, Jacobi sweeps (cumulative, all trees)
-int64_t g_stats[2][19] = {};  // [0] leaf problems, [1] stitch problems
+std::atomic<int64_t> g_stats[2][19] = {};  // [0] leaf problems, [1] stitch problems (concurrent readers)
 
 struct TTError : std::runtime_error {
   tt_status code;
@@ -336,15 +341,29 @@ std::vector<ProblemStatus> run_leaf_batch(Exec& ex, const Params& prm, std::vect
   const int n = static_cast<int>(descs.size());
   std::vector<ProblemStatus> st(static_cast<size_t>(n));
   if (n == 0) return st;
+  // Few problems: one thread-block cluster per problem (leaf_wide_kernel) so a
+  // single streamed leaf or query tail uses 8-16 SMs; wide batches: one CTA
+  // per problem. TT_WIDE=0/1 forces either path (A/B measurement).
+  const int cs = leaf_wide_cluster();
+  bool wide = cs > 0 && prm.p >= 2;
+  if (wide) {
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ex.device);
+    wide = n <= 2 * std::max(1, nsm / cs);
+    if (const char* e = std::getenv("TT_WIDE")) wide = e[0] == '1';
+  }
+  std::vector<Index> wsz(ws_sizes);
+  if (wide)  // + the per-CTA partial Gram slots of the cluster kernel
+    for (int i = 0; i < n; ++i) wsz[i] = leaf_ws_layout(prm.p, descs[i].len, prm.d, prm.req, cs).total;
   size_t ws_total = 0;
-  for (Index w : ws_sizes) ws_total += static_cast<size_t>(w);
+  for (Index w : wsz) ws_total += static_cast<size_t>(w);
   ex.d_ws.ensure(ws_total * sizeof(double));
   ex.d_status.ensure(size_t(n) * kStatusInts * sizeof(int32_t));
   ex.d_obj.ensure(size_t(n) * prm.max_iters * sizeof(double));
   size_t off = 0;
   for (int i = 0; i < n; ++i) {
     descs[i].ws = ex.d_ws.as<double>() + off;
-    off += static_cast<size_t>(ws_sizes[i]);
+    off += static_cast<size_t>(wsz[i]);
     descs[i].status = ex.d_status.as<int32_t>() + size_t(i) * kStatusInts;
     descs[i].objective = ex.d_obj.as<double>() + size_t(i) * prm.max_iters;
   }
@@ -365,17 +384,6 @@ std::vector<ProblemStatus> run_leaf_batch(Exec& ex, const Params& prm, std::vect
   ex.d_desc.ensure(sizeof(LeafDesc) * n);
   cuda_check(cudaMemcpyAsync(ex.d_desc.p, descs.data(), sizeof(LeafDesc) * n, cudaMemcpyHostToDevice, ex.stream),
              "upload leaf descriptors");
-  // Few problems: one thread-block cluster per problem (leaf_wide_kernel) so a
-  // single streamed leaf or query tail uses 8-16 SMs; wide batches: one CTA
-  // per problem. TT_WIDE=0/1 forces either path (A/B measurement).
-  const int cs = leaf_wide_cluster();
-  bool wide = cs > 0 && prm.p >= 2;
-  if (wide) {
-    int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ex.device);
-    wide = n <= 2 * std::max(1, nsm / cs);
-    if (const char* e = std::getenv("TT_WIDE")) wide = e[0] == '1';
-  }
   if (wide)
     cuda_check(launch_leaf_wide(prm, ex.d_desc.as<LeafDesc>(), n, cs, ex.stream), "leaf_wide_kernel launch");
   else
@@ -509,8 +517,10 @@ struct InitCache {
   uint64_t seed = 0;
   std::map<Index, std::vector<std::unique_ptr<DevBuf>>> leaf;  // by block length
   std::vector<std::unique_ptr<DevBuf>> stitch;                 // m >= 1 (index m)
+  std::mutex mu;  // concurrent readers fill the caches (map nodes never move)
 
   const std::vector<std::unique_ptr<DevBuf>>& leaf_init(Index len, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(mu);
     auto it = leaf.find(len);
     if (it != leaf.end()) return it->second;
     Index dd[kMaxP], rc[kMaxP];
@@ -530,6 +540,7 @@ struct InitCache {
     return leaf.emplace(len, std::move(v)).first->second;
   }
   void stitch_init(Params& prm, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(mu);
     if (stitch.empty()) {
       std::mt19937_64 rng(seed);
       stitch.resize(static_cast<size_t>(p));
@@ -594,11 +605,33 @@ struct tt_tree {
   DevBuf tail;  // B slices (device)
   InitCache init;
   DevBuf stage;  // host-burst staging
-  DevBuf qout;      // query output staging (host-destination batches)
-  DevBuf qscratch;  // device scratch for outputs the caller did not request
-  DevBuf tailq;  // tail-part scratch for queries
   double timing[3] = {0, 0, 0};
-  mutable std::mutex qmu;
+  uint64_t timing_stamp = 0;
+  mutable std::mutex qmu;  // serialises tt_tree_save
+  // Query contexts: one stream + workspace per calling thread, so any number of
+  // readers run concurrently between appends (sst.hpp:52-53).
+  struct Reader {
+    std::unique_ptr<Exec> ex;
+    DevBuf qout, qscratch, tailq;
+    double timing[3] = {0, 0, 0};
+    uint64_t stamp = 0;
+  };
+  std::mutex rmu;
+  std::map<std::thread::id, std::unique_ptr<Reader>> readers;
+  Reader& reader() {
+    std::lock_guard<std::mutex> lk(rmu);
+    auto& r = readers[std::this_thread::get_id()];
+    if (!r) {
+      r = std::make_unique<Reader>();
+      r->ex = std::make_unique<Exec>(ex->device);
+    }
+    return *r;
+  }
+  Reader* reader_if_any() {
+    std::lock_guard<std::mutex> lk(rmu);
+    auto it = readers.find(std::this_thread::get_id());
+    return it == readers.end() ? nullptr : it->second.get();
+  }
   // Append journal: pre-call copies of the existing nodes an append modifies
   // (at most the root-to-leaf paths), so a failed append can be rolled back.
   Index journal_n0 = -1;
@@ -612,7 +645,7 @@ struct tt_tree {
 
   HostNode& node(Index id) { return nodes[static_cast<size_t>(id - 1)]; }
   const HostNode& node(Index id) const {
-    if (id < 1 || id > static_cast<Index>(nodes.size())) fail(TT_EINVAL, "unknown node id " + std::to_string(id));
+    if (id < 1 || id > static_cast<Index>(nodes.size())) fail(TT_ERANGE, "StreamSegmentTree::node: unknown node id " + std::to_string(id));
     return nodes[static_cast<size_t>(id - 1)];
   }
   Index clamped(int m, Index len) const { return std::min(cfg.ranks[m], m == 0 ? len : d[m]); }
@@ -634,14 +667,18 @@ struct tt_tree {
   }
   Index height() const {
     if (root == 0) return 0;
-    std::function<Index(Index)> depth = [&](Index id) -> Index {
-      const HostNode& v = node(id);
+    // robust to corrupted node tables (from_parts + validate): unknown ids
+    // count as absent, cycles are cut at depth N
+    const Index N = static_cast<Index>(nodes.size());
+    std::function<Index(Index, Index)> depth = [&](Index id, Index lvl) -> Index {
+      if (id < 1 || id > N || lvl > N) return 0;
+      const HostNode& v = nodes[static_cast<size_t>(id - 1)];
       Index best = 0;
-      if (v.left) best = std::max(best, depth(v.left));
-      if (v.right) best = std::max(best, depth(v.right));
+      if (v.left) best = std::max(best, depth(v.left, lvl + 1));
+      if (v.right) best = std::max(best, depth(v.right, lvl + 1));
       return best + 1;
     };
-    return depth(root);
+    return depth(root, 1);
   }
 };
 
@@ -764,6 +801,8 @@ void execute(tt_tree& t, PendingWork& w, const std::vector<const double*>& leaf_
       for (int m = 0; m < t.p; ++m) v.ranks[m] = st[i].k[m];
     }
   }
+  if (!w.leaves.empty() && g_fail_appends.load() > 0 && g_fail_appends.fetch_sub(1) > 0)
+    fail(TT_ECUDA, "injected append failure (tt_debug_fail_appends)");
   cuda_check(cudaEventRecord(ex.ev[1], ex.stream), "event");
   // ---- stitches, level by level (children always complete at a lower level)
   if (!w.stitches.empty()) {
@@ -831,6 +870,7 @@ void execute(tt_tree& t, PendingWork& w, const std::vector<const double*>& leaf_
   t.timing[0] = a;
   t.timing[1] = b;
   t.timing[2] = a + b;
+  t.timing_stamp = next_stamp();
 }
 
 // query.cpp:9-31 plus the leaf-block rule (an overlapping leaf is always a hit).
@@ -881,7 +921,8 @@ struct tt_factors {
 extern "C" {
 
 const char* tt_last_error(void) { return g_err.c_str(); }
-const char* tt_version(void) { return "tucktree_b200 0.1 (sm_100a)"; }
+const char* tt_version(void) { return "tucktree_b200 0.2 (sm_100a)"; }
+void tt_debug_fail_appends(int32_t n) { g_fail_appends.store(n); }
 int64_t tt_kernel_launches(void) { return launches(); }
 void tt_solver_stats(int64_t* out38) {
   for (int k = 0; k < 2; ++k)
@@ -1120,11 +1161,15 @@ tt_status tt_last_redecomposed(const tt_tree* t, int64_t* ids, int64_t cap, int6
 tt_status tt_last_timing(const tt_tree* t, double* ms3) {
   return guarded([&] {
     if (!t || !ms3) fail(TT_EINVAL, "null argument");
-    for (int i = 0; i < 3; ++i) ms3[i] = t->timing[i];
+    // the calling thread's last query if it is newer than the last append
+    const tt_tree::Reader* rd = const_cast<tt_tree*>(t)->reader_if_any();
+    const double* src = (rd && rd->stamp > t->timing_stamp) ? rd->timing : t->timing;
+    for (int i = 0; i < 3; ++i) ms3[i] = src[i];
   });
 }
 
-// sst.cpp:159-295 (structural invariants; leaf length B).
+// sst.cpp:159-295 (structural invariants), in units of the leaf block B
+// (B = 1: the reference's checks and messages verbatim).
 int32_t tt_validate(const tt_tree* t, char* buf, int64_t cap) {
   if (!t) return -1;
   std::vector<std::string> out;
@@ -1132,7 +1177,7 @@ int32_t tt_validate(const tt_tree* t, char* buf, int64_t cap) {
   auto label = [](const HostNode& n) {
     return "node " + std::to_string(n.id) + " [" + std::to_string(n.begin) + "," + std::to_string(n.end) + ")";
   };
-  const Index B = t->B, T = t->leaves * B;
+  const Index B = t->B, T = t->leaves * B;  // the tree covers whole blocks; a raw tail is not in the tree
   auto ceil_log2 = [](Index n) {
     Index l = 0, q = 1;
     while (q < n) {
@@ -1141,66 +1186,101 @@ int32_t tt_validate(const tt_tree* t, char* buf, int64_t cap) {
     }
     return l;
   };
-  if (t->leaves == 0) {
+  auto finish = [&]() {
+    std::string all;
+    for (auto& s : out) all += s + "\n";
+    if (buf && cap > 0) {
+      std::strncpy(buf, all.c_str(), static_cast<size_t>(cap - 1));
+      buf[cap - 1] = '\0';
+    }
+    return static_cast<int32_t>(out.size());
+  };
+  if (T == 0) {
     if (t->root) flag("empty tree has a root");
-  } else if (!t->root) {
+    return finish();
+  }
+  if (!t->root) {
     flag("non-empty tree has no root");
-  } else {
-    const Index N = static_cast<Index>(t->nodes.size());
-    auto valid = [N](Index id) { return id >= 1 && id <= N; };
-    for (const HostNode& v : t->nodes) {
-      if (v.begin < 0 || v.begin >= v.end) flag(label(v) + ": malformed range");
-      if ((v.left && !valid(v.left)) || (v.right && !valid(v.right))) {
-        flag(label(v) + ": child id unknown");
-        continue;
-      }
-      if (v.kind == TT_LEAF) {
-        if (v.length() != B) flag(label(v) + ": leaf range must have length 1");
-        if (v.left || v.right) flag(label(v) + ": leaf must not have children");
-        if (!v.has_dec) flag(label(v) + ": leaf is missing its decomposition");
-      } else if (v.kind == TT_INTERMEDIATE) {
-        if (!v.left || !v.right) {
-          flag(label(v) + ": intermediate must have two children");
-        } else {
-          const HostNode& l = t->node(v.left);
-          const HostNode& r = t->node(v.right);
-          if (l.begin != v.begin || l.end != r.begin || r.end != v.end) flag(label(v) + ": children ranges are not adjoint");
-          if (l.kind == TT_PLACEHOLDER || r.kind == TT_PLACEHOLDER) flag(label(v) + ": intermediate has a placeholder child");
-          if (!v.has_dec) flag(label(v) + ": intermediate is missing its decomposition");
-        }
+    return finish();
+  }
+  const Index N = static_cast<Index>(t->nodes.size());
+  auto valid = [N](Index id) { return id >= 1 && id <= N; };
+  const std::string leaf_len = B == 1 ? "1" : std::to_string(B);
+  for (const HostNode& v : t->nodes) {
+    if (v.begin < 0 || v.begin >= v.end) flag(label(v) + ": malformed range");
+    if ((v.left && !valid(v.left)) || (v.right && !valid(v.right))) {
+      flag(label(v) + ": child id unknown");
+      continue;
+    }
+    if (v.kind == TT_LEAF) {
+      if (v.length() != B) flag(label(v) + ": leaf range must have length " + leaf_len);
+      if (v.left || v.right) flag(label(v) + ": leaf must not have children");
+      if (!v.has_dec) flag(label(v) + ": leaf is missing its decomposition");
+    } else if (v.kind == TT_INTERMEDIATE) {
+      if (!v.left || !v.right) {
+        flag(label(v) + ": intermediate must have two children");
       } else {
-        if (v.has_dec) flag(label(v) + ": placeholder carries a decomposition");
-        if (!(v.begin < T && T <= v.end)) flag(label(v) + ": placeholder does not straddle the write frontier");
-        if (!v.left && v.right) flag(label(v) + ": placeholder has a right child without a left child");
-        if (!v.left && !v.right) flag(label(v) + ": placeholder has no children");
+        const HostNode& l = t->node(v.left);
+        const HostNode& r = t->node(v.right);
+        if (l.begin != v.begin || l.end != r.begin || r.end != v.end) flag(label(v) + ": children ranges are not adjoint");
+        if (l.kind == TT_PLACEHOLDER || r.kind == TT_PLACEHOLDER) flag(label(v) + ": intermediate has a placeholder child");
+        if (!v.has_dec) flag(label(v) + ": intermediate is missing its decomposition");
       }
-      if (v.kind != TT_PLACEHOLDER && v.end > T) flag(label(v) + ": materialized node extends past the timespan");
-    }
-    std::vector<const HostNode*> lv;
-    for (const HostNode& v : t->nodes)
-      if (v.kind == TT_LEAF) lv.push_back(&v);
-    std::sort(lv.begin(), lv.end(), [](const HostNode* a, const HostNode* b) { return a->begin < b->begin; });
-    Index expected = 0;
-    for (const HostNode* l : lv) {
-      if (l->begin != expected) {
-        flag(label(*l) + ": leaf tiling gap or overlap");
-        break;
+    } else if (v.kind == TT_PLACEHOLDER) {
+      if (v.has_dec) flag(label(v) + ": placeholder carries a decomposition");
+      if (!(v.begin < T && T <= v.end)) flag(label(v) + ": placeholder does not straddle the write frontier");
+      if (!v.left && v.right) flag(label(v) + ": placeholder has a right child without a left child");
+      if (!v.left && !v.right) flag(label(v) + ": placeholder has no children");
+      if (v.left && v.right) {
+        const HostNode& l = t->node(v.left);
+        const HostNode& r = t->node(v.right);
+        if (l.begin != v.begin || l.end != r.begin || r.end != v.end) flag(label(v) + ": children ranges are not adjoint");
+      } else if (v.left) {
+        const HostNode& l = t->node(v.left);
+        // midpoint split in leaf units (sst.cpp:119: mid = (b + e) / 2)
+        const Index mid = ((v.begin / B + v.end / B) / 2) * B;
+        if (l.begin != v.begin || l.end != mid) flag(label(v) + ": left child range does not match the midpoint split");
       }
-      expected = l->end;
+    } else {
+      flag(label(v) + ": unknown node kind");
     }
-    if (expected != T && out.empty()) flag("leaves do not cover the timespan");
-    const HostNode& r = t->node(t->root);
-    const Index span = (t->leaves == 1 ? 1 : (Index(1) << ceil_log2(t->leaves))) * B;
-    if (r.begin != 0 || r.end != span) flag(label(r) + ": root range wrong");
-    if (t->height() != ceil_log2(t->leaves) + 1) flag("height violates the height law");
+    if (v.kind != TT_PLACEHOLDER && v.end > T) flag(label(v) + ": materialized node extends past the timespan");
+    if (v.has_dec && !t->structure_only) {
+      // the device slots hold factor 0 with the node's length rows and factor m
+      // with D_m rows; the core extents are the factor column counts
+      for (int m = 0; m < t->p; ++m)
+        if (v.ranks[m] < 1 || v.ranks[m] > t->clamped(m, v.length())) {
+          flag(label(v) + ": core extent does not match factor columns");
+          break;
+        }
+    }
   }
-  std::string all;
-  for (auto& s : out) all += s + "\n";
-  if (buf && cap > 0) {
-    std::strncpy(buf, all.c_str(), static_cast<size_t>(cap - 1));
-    buf[cap - 1] = '\0';
+  std::vector<const HostNode*> lv;
+  for (const HostNode& v : t->nodes)
+    if (v.kind == TT_LEAF) lv.push_back(&v);
+  std::sort(lv.begin(), lv.end(), [](const HostNode* a, const HostNode* b) { return a->begin < b->begin; });
+  Index expected = 0;
+  for (const HostNode* l : lv) {
+    if (l->begin != expected) {
+      flag(label(*l) + ": leaf tiling gap or overlap at " + std::to_string(expected));
+      break;
+    }
+    expected = l->end;
   }
-  return static_cast<int32_t>(out.size());
+  if (expected != T && out.empty())
+    flag("leaves cover [0," + std::to_string(expected) + ") but timespan is " + std::to_string(T));
+  if (!valid(t->root)) {
+    flag("root id unknown");
+    return finish();
+  }
+  const HostNode& r = t->node(t->root);
+  const Index nl = T / B;
+  const Index span = (nl == 1 ? 1 : (Index(1) << ceil_log2(nl))) * B;
+  if (r.begin != 0 || r.end != span) flag(label(r) + ": root range should be [0," + std::to_string(span) + ")");
+  const Index eh = ceil_log2(nl) + 1;
+  if (t->height() != eh)
+    flag("height " + std::to_string(t->height()) + " violates the height law " + std::to_string(eh));
+  return finish();
 }
 
 tt_status tt_recall(const tt_tree* t, int64_t ts, int64_t te, double theta, tt_hit* out, int64_t cap, int64_t* n) {
@@ -1220,12 +1300,12 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
     if (n <= 0) return;
     if (!ranges || !outs) fail(TT_EINVAL, "null ranges/outs");
     if (t->structure_only) fail(TT_ELOGIC, "range_query on a structure-only tree");
-    std::lock_guard<std::mutex> lk(t->qmu);
     const int p = t->p;
     // recall for every query first: an invalid range fails the batch before any device work
     std::vector<std::vector<tt_hit>> hits(static_cast<size_t>(n));
     for (int64_t q = 0; q < n; ++q) hits[q] = recall(*t, ranges[q].ts, ranges[q].te, theta);
-    Exec& ex = *t->ex;
+    tt_tree::Reader& rd = t->reader();
+    Exec& ex = *rd.ex;
     DeviceGuard g(ex.device);
     Params prm = tree_params(*t);
     t->init.stitch_init(prm, ex.stream);
@@ -1255,8 +1335,8 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
         need += 64 * static_cast<size_t>(p);
       }
       if (!tl.empty()) {
-        t->tailq.ensure(need * sizeof(double));
-        double* cur = t->tailq.as<double>();
+        rd.tailq.ensure(need * sizeof(double));
+        double* cur = rd.tailq.as<double>();
         auto take = [&cur](Index nd) {
           double* r = cur;
           cur += (nd + 31) & ~Index(31);
@@ -1402,9 +1482,9 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
           stage_off[idx[i]] = off;
           off += (orefs[idx[i]].bytes + 7) & ~size_t(7);
         }
-        t->qout.ensure(std::max<size_t>(off, 8));
+        rd.qout.ensure(std::max<size_t>(off, 8));
         for (size_t i = 0; i < orefs.size(); ++i) {
-          double* dptr = reinterpret_cast<double*>(t->qout.as<char>() + stage_off[i]);
+          double* dptr = reinterpret_cast<double*>(rd.qout.as<char>() + stage_off[i]);
           StitchDesc& dsc = descs[orefs[i].q];
           if (orefs[i].m < 0)
             dsc.out_core = dptr;
@@ -1422,8 +1502,8 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
             if (!outs[q].factors[m]) extra += static_cast<size_t>((m == 0 ? L : t->d[m]) * rc[m]);
         }
         if (extra) {
-          t->qscratch.ensure(extra * sizeof(double));
-          double* cur = t->qscratch.as<double>();
+          rd.qscratch.ensure(extra * sizeof(double));
+          double* cur = rd.qscratch.as<double>();
           for (int64_t q = q0; q < q1; ++q) {
             const Index L = descs[q - q0].L;
             Index rc[kMaxP];
@@ -1441,7 +1521,7 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
           }
         }
       } else {
-        if (where == TT_MEM_HOST) t->qout.ensure(out_need * sizeof(double));
+        if (where == TT_MEM_HOST) rd.qout.ensure(out_need * sizeof(double));
         double* dscr = nullptr;  // device scratch for outputs the caller did not request (null pointers)
         if (where == TT_MEM_DEVICE) {
           size_t extra = 0;
@@ -1452,8 +1532,8 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
               if (!outs[q].factors[m]) extra += static_cast<size_t>((m == 0 ? L : t->d[m]) * t->clamped(m, L)) + 32;
           }
           if (extra) {
-            t->qscratch.ensure(extra * sizeof(double));
-            dscr = t->qscratch.as<double>();
+            rd.qscratch.ensure(extra * sizeof(double));
+            dscr = rd.qscratch.as<double>();
           }
         }
         for (int64_t q = q0; q < q1; ++q) {
@@ -1471,7 +1551,7 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
               dsc.out_f[m] = outs[q].factors[m] ? outs[q].factors[m] : scratch((m == 0 ? L : t->d[m]) * rc[m]);
             dsc.out_core = outs[q].core ? outs[q].core : scratch(prod_range(t->cfg.ranks, 0, p));
           } else {
-            double* cur = t->qout.as<double>() + out_off[q - q0];
+            double* cur = rd.qout.as<double>() + out_off[q - q0];
             auto take = [&cur](Index nd) {
               double* r = cur;
               cur += (nd + 31) & ~Index(31);
@@ -1561,7 +1641,7 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
               len += orefs[wr[r2]].bytes;
               ++r2;
             }
-            cuda_check(cudaMemcpyAsync(h0, t->qout.as<char>() + s0, len, cudaMemcpyDeviceToHost, ex.copy),
+            cuda_check(cudaMemcpyAsync(h0, rd.qout.as<char>() + s0, len, cudaMemcpyDeviceToHost, ex.copy),
                        "query output download");
             r = r2;
           }
@@ -1594,6 +1674,11 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
         o.converged = s.converged;
         o.objective = s.objective.empty() ? 0.0 : s.objective.back();
         o.nhits = static_cast<int32_t>(hits[q].size());
+        if (o.trace && o.trace_cap > 0)  // AlsTrace::objective (range_query_detailed, query.hpp:48-50)
+          for (size_t i = 0; i < s.objective.size() && static_cast<int32_t>(i) < o.trace_cap; ++i)
+            o.trace[i] = s.objective[i];
+        if (o.hits && o.hits_cap > 0)  // QueryResult::hits
+          for (size_t i = 0; i < hits[q].size() && static_cast<int32_t>(i) < o.hits_cap; ++i) o.hits[i] = hits[q][i];
         if (where == TT_MEM_HOST && !dma) {
           const StitchDesc& dsc = descs[q - q0];
           // small outputs: one gather kernel into mapped host memory when every
@@ -1633,9 +1718,10 @@ tt_status tt_query_batch(const tt_tree* tc, const tt_range* ranges, int64_t n, d
     float a = 0, b = 0;
     cudaEventElapsedTime(&a, ex.ev[0], ex.ev[1]);
     cudaEventElapsedTime(&b, ex.ev[1], ex.ev[2]);
-    t->timing[0] = a;
-    t->timing[1] = b;
-    t->timing[2] = a + b;
+    rd.timing[0] = a;
+    rd.timing[1] = b;
+    rd.timing[2] = a + b;
+    rd.stamp = next_stamp();
   });
 }
 
@@ -2106,6 +2192,82 @@ void write_node_factors(Writer& w, const tt_tree& t, const HostNode& v) {
 
 }  // namespace
 
+namespace {
+// A node record with its host payload (SST1 reader, from_parts).
+struct PartRec {
+  HostNode v;
+  std::vector<double> core;
+  std::vector<std::vector<double>> f;  // column-major
+};
+
+// StreamSegmentTree::from_parts (sst.cpp:30-71): ids are creation order
+// 1..n, children exist; payloads are uploaded into the tree's device slots.
+// `code` is the status for malformed records (TT_EIO for files).
+tt_tree* install_parts(tt_config cfg, std::vector<PartRec>& recs, Index root, Index timespan, Index stitches,
+                       Index tail, const std::vector<double>& tail_buf, tt_status code) {
+  const int p = cfg.order;
+  const Index B = std::max<Index>(cfg.leaf_block, 1);
+  const uint64_t count = recs.size();
+  tt_tree* raw = nullptr;
+  const tt_status st = tt_tree_create(&cfg, &raw);
+  if (st != TT_OK) fail(st, g_err);
+  std::unique_ptr<tt_tree, void (*)(tt_tree*)> t(raw, tt_tree_destroy);
+  // A file (strict) must be a consistent tree; from_parts (sst.cpp:47-62) only
+  // checks the id order and the root id — the rest is validate()'s job.
+  const bool strict = code == TT_EIO;
+  Index leaves = 0;
+  for (uint64_t i = 0; i < count; ++i) {
+    const HostNode& v = recs[i].v;
+    if (v.id != static_cast<Index>(i + 1))
+      fail(code, strict ? "node ids must be 1..n in creation order" : "from_parts: node ids must be 1..N in order");
+    if (!strict) continue;
+    if (v.left > static_cast<Index>(count) || v.right > static_cast<Index>(count) || v.left < 0 || v.right < 0)
+      fail(code, "node child id out of range");
+    if (v.begin < 0 || v.end <= v.begin || v.end % B != 0 || v.begin % B != 0)
+      fail(code, "node range not aligned to the leaf block");
+    if (v.kind == TT_LEAF) ++leaves;
+  }
+  if (root < 0 || root > static_cast<Index>(count))
+    fail(code, strict ? "root id out of range" : "from_parts: root id out of range");
+  if (!strict) leaves = timespan / B;
+  if (timespan != leaves * B + tail) fail(code, "timespan does not match the leaves and tail");
+  t->nodes.reserve(static_cast<size_t>(count));
+  for (PartRec& rc : recs) {
+    HostNode v = rc.v;
+    v.core = nullptr;
+    for (int m = 0; m < kMaxP; ++m) v.f[m] = nullptr;
+    t->nodes.push_back(v);
+    HostNode& dv = t->nodes.back();
+    if (!dv.has_dec || t->structure_only) continue;
+    for (int m = 0; m < p; ++m)
+      if (dv.ranks[m] > t->clamped(m, std::max<Index>(dv.length(), 1)))
+        fail(code, "node rank exceeds the tree's (clamped) ranks: the device slots are sized by them");
+    if (dv.length() < 1) fail(code, "a node with a decomposition needs a non-empty range");
+    t->alloc_slots(dv);
+    DeviceGuard g(t->ex->device);
+    cuda_check(cudaMemcpyAsync(dv.core, rc.core.data(), rc.core.size() * sizeof(double), cudaMemcpyHostToDevice,
+                               t->ex->stream),
+               "node core upload");
+    for (int m = 0; m < p; ++m)
+      cuda_check(cudaMemcpyAsync(dv.f[m], rc.f[m].data(), rc.f[m].size() * sizeof(double), cudaMemcpyHostToDevice,
+                                 t->ex->stream),
+                 "node factor upload");
+    t->ex->sync();  // host staging buffers are freed per node
+  }
+  t->root = root;
+  t->timespan = timespan;
+  t->leaves = leaves;
+  t->stitch_count = stitches;
+  t->last_touches = 0;
+  if (tail > 0 && !t->structure_only) {
+    DeviceGuard g(t->ex->device);
+    cuda_check(cudaMemcpy(t->tail.p, tail_buf.data(), tail_buf.size() * sizeof(double), cudaMemcpyHostToDevice),
+               "tail upload");
+  }
+  return t.release();
+}
+}  // namespace
+
 extern "C" {
 
 tt_status tt_tree_save(const tt_tree* t, const char* path) {
@@ -2181,14 +2343,9 @@ tt_status tt_tree_load(const char* path, int32_t device, int32_t flags, tt_tree*
     const uint64_t root = r.le<uint64_t>("root id");
     const uint64_t count = r.le<uint64_t>("node count");
     if (count > (uint64_t(1) << 32)) fail(TT_EIO, "implausible node count");
-    struct Rec {
-      HostNode v;
-      std::vector<double> core;
-      std::vector<std::vector<double>> f;  // column-major
-    };
-    std::vector<Rec> recs(static_cast<size_t>(count));
+    std::vector<PartRec> recs(static_cast<size_t>(count));
     for (uint64_t i = 0; i < count; ++i) {
-      Rec& rc = recs[i];
+      PartRec& rc = recs[i];
       HostNode& v = rc.v;
       v.id = static_cast<Index>(r.le<uint64_t>("node id"));
       v.begin = static_cast<Index>(r.le<uint64_t>("node range"));
@@ -2241,55 +2398,57 @@ tt_status tt_tree_load(const char* path, int32_t device, int32_t flags, tt_tree*
     cfg.leaf_block = B;
     cfg.device = device;
     cfg.flags = flags;
-    tt_tree* raw = nullptr;
-    const tt_status st = tt_tree_create(&cfg, &raw);
-    if (st != TT_OK) fail(st, g_err);
-    std::unique_ptr<tt_tree, void (*)(tt_tree*)> t(raw, tt_tree_destroy);
-    // from_parts (sst.cpp:30-71): ids are creation order 1..n, children exist
-    Index leaves = 0;
-    for (uint64_t i = 0; i < count; ++i) {
-      const HostNode& v = recs[i].v;
-      if (v.id != static_cast<Index>(i + 1)) fail(TT_EIO, "node ids must be 1..n in creation order");
-      if (v.left > static_cast<Index>(count) || v.right > static_cast<Index>(count) || v.left < 0 || v.right < 0)
-        fail(TT_EIO, "node child id out of range");
-      if (v.begin < 0 || v.end <= v.begin || v.end % B != 0 || v.begin % B != 0)
-        fail(TT_EIO, "node range not aligned to the leaf block");
-      if (v.kind == TT_LEAF) ++leaves;
+    *out = install_parts(cfg, recs, static_cast<Index>(root), static_cast<Index>(timespan),
+                         static_cast<Index>(stitches), tail, tail_buf, TT_EIO);
+  });
+}
+
+tt_status tt_tree_from_parts(const tt_config* cfg, const tt_node_info* nodes, int64_t n, const double* const* cores,
+                             const double* const* factors, int64_t root, int64_t timespan, int64_t stitch_count,
+                             tt_tree** out) {
+  return guarded([&] {
+    if (!cfg || !out || (n > 0 && !nodes)) fail(TT_EINVAL, "from_parts: null argument");
+    if (n < 0) fail(TT_EINVAL, "from_parts: negative node count");
+    *out = nullptr;
+    const int p = cfg->order;
+    if (p < 2 || p > TT_MAX_ORDER) fail(TT_EINVAL, "StreamSegmentTree: order must be in [2, 8]");
+    std::vector<PartRec> recs(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      PartRec& rc = recs[static_cast<size_t>(i)];
+      const tt_node_info& ni = nodes[i];
+      if (ni.kind < 0 || ni.kind > 2) fail(TT_EINVAL, "from_parts: invalid node kind");
+      rc.v.id = ni.id;
+      rc.v.begin = ni.begin;
+      rc.v.end = ni.end;
+      rc.v.kind = ni.kind;
+      rc.v.left = ni.left;
+      rc.v.right = ni.right;
+      if (!ni.has_decomposition) continue;
+      if (cfg->flags & TT_FLAG_STRUCTURE_ONLY) {  // bookkeeping only: the flag without a payload
+        rc.v.has_dec = true;
+        for (int m = 0; m < p; ++m) rc.v.ranks[m] = ni.ranks[m];
+        continue;
+      }
+      if (!cores || !factors || !cores[i]) fail(TT_EINVAL, "from_parts: missing decomposition payload");
+      Index cd[kMaxP];
+      for (int m = 0; m < p; ++m) {
+        cd[m] = ni.ranks[m];
+        if (cd[m] < 1) fail(TT_EINVAL, "from_parts: decomposition ranks must be >= 1");
+        rc.v.ranks[m] = cd[m];
+      }
+      rc.core.assign(cores[i], cores[i] + prod_range(cd, 0, p));
+      rc.f.resize(static_cast<size_t>(p));
+      for (int m = 0; m < p; ++m) {
+        const double* fm = factors[i * p + m];
+        if (!fm) fail(TT_EINVAL, "from_parts: missing factor payload");
+        const Index rows = m == 0 ? ni.end - ni.begin : cfg->nontemporal[m - 1];
+        rc.f[m].assign(fm, fm + rows * cd[m]);
+      }
+      rc.v.has_dec = true;
     }
-    if (root > count) fail(TT_EIO, "root id out of range");
-    if (static_cast<Index>(timespan) != leaves * B + tail) fail(TT_EIO, "timespan does not match the leaves and tail");
-    t->nodes.reserve(static_cast<size_t>(count));
-    for (Rec& rc : recs) {
-      HostNode v = rc.v;
-      v.core = nullptr;
-      for (int m = 0; m < kMaxP; ++m) v.f[m] = nullptr;
-      t->nodes.push_back(v);
-      HostNode& dv = t->nodes.back();
-      if (!dv.has_dec || t->structure_only) continue;
-      for (int m = 0; m < p; ++m)
-        if (dv.ranks[m] > t->clamped(m, dv.length())) fail(TT_EIO, "node rank exceeds the tree's ranks");
-      t->alloc_slots(dv);
-      DeviceGuard g(t->ex->device);
-      cuda_check(cudaMemcpyAsync(dv.core, rc.core.data(), rc.core.size() * sizeof(double), cudaMemcpyHostToDevice,
-                                 t->ex->stream),
-                 "node core upload");
-      for (int m = 0; m < p; ++m)
-        cuda_check(cudaMemcpyAsync(dv.f[m], rc.f[m].data(), rc.f[m].size() * sizeof(double), cudaMemcpyHostToDevice,
-                                   t->ex->stream),
-                   "node factor upload");
-      t->ex->sync();  // host staging buffers are freed per node
-    }
-    t->root = static_cast<Index>(root);
-    t->timespan = static_cast<Index>(timespan);
-    t->leaves = leaves;
-    t->stitch_count = static_cast<Index>(stitches);
-    t->last_touches = 0;
-    if (tail > 0 && !t->structure_only) {
-      DeviceGuard g(t->ex->device);
-      cuda_check(cudaMemcpy(t->tail.p, tail_buf.data(), tail_buf.size() * sizeof(double), cudaMemcpyHostToDevice),
-                 "tail upload");
-    }
-    *out = t.release();
+    const Index B = std::max<Index>(cfg->leaf_block, 1);
+    if (timespan % B != 0) fail(TT_EINVAL, "from_parts: timespan must be a multiple of the leaf block");
+    *out = install_parts(*cfg, recs, root, timespan, stitch_count, 0, {}, TT_EINVAL);
   });
 }
 

@@ -1197,9 +1197,16 @@ cudaError_t launch_copy_segments(const CopySeg* d_segs, int n, cudaStream_t st) 
 cudaError_t launch_stitch(const Params& prm, const StitchDesc* d_descs, const StitchPart* d_parts, int n,
                           cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  const cudaError_t ae = ensure_dyn_smem(reinterpret_cast<const void*>(stitch_als_kernel), 1, kDynSmem);
+  // Batches that leave most SMs idle (streamed appends, single queries) run one
+  // CTA per SM with 200 KB of dynamic shared memory: the solvers then keep
+  // their 100 x 100 Grams and iteration state on chip (sc.dsm_cap adapts).
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const size_t dyn = n <= nsm ? kDynSmemSolo : kDynSmem;
+  const cudaError_t ae = ensure_dyn_smem(reinterpret_cast<const void*>(stitch_als_kernel), 1, kDynSmemSolo);
   if (ae != cudaSuccess) return ae;
-  stitch_als_kernel<<<n, kStitchThreads, kDynSmem, st>>>(prm, d_descs, d_parts);
+  stitch_als_kernel<<<n, kStitchThreads, dyn, st>>>(prm, d_descs, d_parts);
   g_launches.fetch_add(1);
   return cudaGetLastError();
 }

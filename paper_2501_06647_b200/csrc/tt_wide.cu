@@ -233,6 +233,55 @@ __device__ __forceinline__ void mode_product_cl(const double* in, int64_t outer,
   __syncthreads();
 }
 
+// leading_left_singular_vectors (linalg.cpp:45-64) of the mode unfolding of a
+// row-major (outer, rows, inner) tensor for the cluster: when llsv_unfold
+// takes its Gram route with a tiled Gram, every CTA forms the Gram over its
+// share of the long side into its partial slot, and the leader sums the
+// partials in rank order and runs the solver; otherwise the leader does it
+// all. Called by every CTA of the cluster (one cluster barrier inside on the
+// distributed route); U is valid on the leader afterwards.
+__device__ void wide_llsv(const double* P, int64_t outer, int64_t rows, int64_t inner, int64_t k, double* U,
+                          double* G, double* V, double* misc, double* dsm, BlockScratch& sc, int64_t kprev,
+                          double* si, double* gpart, int rank, int CS) {
+  const int64_t cols = outer * inner;
+  const bool wide = rows <= cols;
+  const int n = int(wide ? rows : cols);
+  const bool dist = CS > 1 && !llsv_uses_subspace(rows, cols, k, kprev, si, sc) && n >= kGramTiledMinN &&
+                    n * 4 <= sc.dsm_cap;
+  if (!dist) {
+    if (rank == 0) llsv_unfold(P, outer, rows, inner, k, U, G, V, misc, dsm, sc, kprev, si);
+    return;
+  }
+  const long long tg = tstart();
+  const int64_t nx = wide ? cols : rows;
+  const int64_t per = (nx + CS - 1) / CS;
+  const int64_t x0 = imin(nx, int64_t(rank) * per), x1 = imin(nx, x0 + per);
+  double* Gp = gpart + int64_t(rank) * n * n;
+  auto unf = [&](int64_t i, int64_t c) {
+    const int64_t o = c / inner, t = c - o * inner;
+    return P[(o * rows + i) * inner + t];
+  };
+  if (x1 <= x0) {
+    for (int64_t idx = threadIdx.x; idx < int64_t(n) * n; idx += blockDim.x) Gp[idx] = 0.0;
+    __syncthreads();
+  } else if (wide) {  // G = A A^T: x over the columns
+    gram_tiled(n, x1 - x0, [&](int64_t c, int a) { return unf(a, x0 + c); }, true, Gp, dsm, sc.dsm_cap);
+  } else {  // G = A^T A: x over the rows
+    gram_tiled(n, x1 - x0, [&](int64_t i, int a) { return unf(x0 + i, a); }, false, Gp, dsm, sc.dsm_cap);
+  }
+  cl_sync();
+  if (rank == 0) {
+    for (int64_t idx = threadIdx.x; idx < int64_t(n) * n; idx += blockDim.x) {
+      double v = 0.0;
+      for (int r = 0; r < CS; ++r) v += gpart[int64_t(r) * n * n + idx];
+      G[idx] = v;
+    }
+    __syncthreads();
+    tstop(sc, kPhGram, tg);
+    llsv_unfold(P, outer, rows, inner, k, U, G, V, misc, dsm, sc, kprev, si, /*gram_ready=*/true);
+  }
+}
+
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads, 1) leaf_wide_kernel(Params prm, const LeafDesc* __restrict__ descs) {
   __shared__ BlockScratch sc;
@@ -258,8 +307,9 @@ __global__ void __launch_bounds__(kThreads, 1) leaf_wide_kernel(Params prm, cons
   d[0] = D.len;
   for (int m = 1; m < p; ++m) d[m] = prm.d[m];
   clamp_ranks(p, d, prm.req, rc);
-  const LeafWs lay = leaf_ws_layout(p, D.len, prm.d, prm.req);
+  const LeafWs lay = leaf_ws_layout(p, D.len, prm.d, prm.req, CS);
   double* W = D.ws + lay.W;
+  double* gpart = D.ws + lay.gpart;
   double* B[2] = {D.ws + lay.B1, D.ws + lay.B2};
   double* G = D.ws + lay.G;
   double* V = D.ws + lay.V;
@@ -322,8 +372,8 @@ __global__ void __launch_bounds__(kThreads, 1) leaf_wide_kernel(Params prm, cons
       }
       norm = sqrt(norm_sq);
     }
-    if (leader)
-      llsv_unfold(src, 1, d[0], prod_range(cur, 1, p), k0n, D.out_f[0], G, V, misc, dsm, sc, k[0], D.ws + lay.SI);
+    wide_llsv(src, 1, d[0], prod_range(cur, 1, p), k0n, D.out_f[0], G, V, misc, dsm, sc, k[0], D.ws + lay.SI, gpart,
+              rank, CS);
     k[0] = k0n;
     cl_sync();
     // ---- W = X x_0 U_0^T : (k0, D_1, ..., D_{p-1}), split
@@ -358,9 +408,8 @@ __global__ void __launch_bounds__(kThreads, 1) leaf_wide_kernel(Params prm, cons
         s2 = dst;
         t2 ^= 1;
       }
-      if (leader)
-        llsv_unfold(s2, prod_range(pc, 0, n), d[n], prod_range(pc, n + 1, p), kn, D.out_f[n], G, V, misc, dsm, sc,
-                    k[n], D.ws + lay.SI);
+      wide_llsv(s2, prod_range(pc, 0, n), d[n], prod_range(pc, n + 1, p), kn, D.out_f[n], G, V, misc, dsm, sc, k[n],
+                D.ws + lay.SI, gpart, rank, CS);
       k[n] = kn;
       Pn = s2;
       cl_sync();

@@ -53,7 +53,8 @@ class TTRange(C.Structure):
 
 class TTQueryOut(C.Structure):
     _fields_ = [("core", dptr), ("factors", dptr * MAX_ORDER), ("ranks", C.c_int64 * MAX_ORDER), ("sweeps", C.c_int32),
-                ("converged", C.c_int32), ("objective", C.c_double), ("nhits", C.c_int32), ("pad", C.c_int32)]
+                ("converged", C.c_int32), ("objective", C.c_double), ("nhits", C.c_int32), ("trace_cap", C.c_int32),
+                ("trace", dptr), ("hits", C.POINTER(TTHit)), ("hits_cap", C.c_int32), ("pad", C.c_int32)]
 
 
 _lib = None
@@ -66,6 +67,9 @@ SIGNATURES = {
     "tt_tree_create": (C.c_int, [C.POINTER(TTConfig), C.POINTER(vp)]),
     "tt_tree_destroy": (None, [vp]),
     "tt_tree_clear": (C.c_int, [vp]),
+    "tt_debug_fail_appends": (None, [C.c_int32]),
+    "tt_tree_from_parts": (C.c_int, [C.POINTER(TTConfig), C.POINTER(TTNodeInfo), i64, C.POINTER(dptr), C.POINTER(dptr),
+                                     i64, i64, i64, C.POINTER(vp)]),
     "tt_append": (C.c_int, [vp, dptr, i64, C.c_int]),
     "tt_tree_stat": (i64, [vp, C.c_int32]),
     "tt_node_info_get": (C.c_int, [vp, i64, C.POINTER(TTNodeInfo)]),
@@ -140,6 +144,10 @@ class IOError_(TuckTreeError, RuntimeError):
     """std::runtime_error from the reference's I/O layer (io.cpp:19)."""
 
 
+class OutOfRange(LogicError, IndexError):
+    """std::out_of_range (a std::logic_error): unknown node id (sst.cpp:68)."""
+
+
 def _check(code: int):
     if code == 0:
         return
@@ -152,6 +160,8 @@ def _check(code: int):
         raise IOError_(msg)
     if code == 4:
         raise CudaError(msg)
+    if code == 7:
+        raise OutOfRange(msg)
     raise TuckTreeError(f"status {code}: {msg}")
 
 
@@ -445,7 +455,8 @@ class StreamSegmentTree:
         _check(lib().tt_recall(self._h, ts, te, float('nan') if theta is None else theta, out, cap, C.byref(n)))
         return [HitEntry(out[i].node, out[i].begin, out[i].end, out[i].flag) for i in range(n.value)]
 
-    def range_query_batch(self, ranges, theta: Optional[float] = None, return_info: bool = False):
+    def range_query_batch(self, ranges, theta: Optional[float] = None, return_info: bool = False,
+                          detailed: bool = False):
         """range_query for many [ts, te) at once (one batched GPU launch)."""
         ranges = [(int(a), int(b)) for a, b in ranges]
         n = len(ranges)
@@ -460,27 +471,87 @@ class StreamSegmentTree:
             core = np.zeros(int(np.prod(rc)))
             rows = [L] + list(self.nontemporal)
             fs = [np.zeros(rows[m] * rc[m]) for m in range(p)]
-            keep.append((core, fs, rows))
+            tr = np.zeros(max(self.max_iters, 1))
+            keep.append((core, fs, rows, tr))
             outs[i].core = _d(core)
             for m in range(p):
                 outs[i].factors[m] = _d(fs[m])
+            outs[i].trace, outs[i].trace_cap = _d(tr), len(tr)  # AlsTrace::objective per sweep
+            if detailed:  # QueryResult::hits, filled by the same call (no second recall)
+                hb = (TTHit * 256)()
+                keep[-1] = keep[-1] + (hb,)
+                outs[i].hits, outs[i].hits_cap = C.cast(hb, C.POINTER(TTHit)), 256
         _check(lib().tt_query_batch(self._h, rr, n, float('nan') if theta is None else theta, outs, TT_MEM_HOST))
         res = []
         for i in range(n):
-            core, fs, rows = keep[i]
+            core, fs, rows, tr = keep[i][:4]
             k = [outs[i].ranks[m] for m in range(p)]
             f = TuckerFactors(core[: int(np.prod(k))].reshape(k),
                               [fs[m][: rows[m] * k[m]].reshape(k[m], rows[m]).T.copy() for m in range(p)],
-                              [outs[i].objective], bool(outs[i].converged), outs[i].sweeps)
-            res.append((f, outs[i].nhits) if return_info else f)
+                              [float(v) for v in tr[: outs[i].sweeps]], bool(outs[i].converged), outs[i].sweeps)
+            if detailed:
+                hb = keep[i][4]
+                hits = [HitEntry(hb[j].node, hb[j].begin, hb[j].end, hb[j].flag) for j in range(min(outs[i].nhits, 256))]
+                res.append(QueryResult(f, hits))
+            else:
+                res.append((f, outs[i].nhits) if return_info else f)
         return res
 
     def range_query(self, ts: int, te: int, theta: Optional[float] = None) -> TuckerFactors:
         return self.range_query_batch([(ts, te)], theta)[0]
 
     def range_query_detailed(self, ts: int, te: int, theta: Optional[float] = None) -> QueryResult:
-        hits = self.recall(ts, te, theta)
-        return QueryResult(self.range_query(ts, te, theta), hits)
+        """range_query_detailed (query.hpp:48-50): factors with the per-sweep
+        objective trace (AlsTrace) in .objective, plus the hit set used."""
+        return self.range_query_batch([(ts, te)], theta, detailed=True)[0]
+
+    @classmethod
+    def from_parts(cls, nontemporal, ranks, nodes, root: int, timespan: int, stitch_count: int,
+                   decompositions: Optional[dict] = None, theta: float = 0.7, max_iters: int = 20, tol: float = 0.01,
+                   seed: int = kDefaultSeed, leaf_block: int = 1, device: int = 0) -> "StreamSegmentTree":
+        """StreamSegmentTree::from_parts (sst.hpp:58-62): ids must be 1..N in order and
+        root in [0, N]; other invariants are validate()'s job. decompositions maps a
+        node id to its TuckerFactors (for nodes with has_decomposition)."""
+        decompositions = decompositions or {}
+        p = len(ranks)
+        cfg = TTConfig()
+        cfg.order = p
+        for m, dm in enumerate(nontemporal):
+            cfg.nontemporal[m] = int(dm)
+        for m, r in enumerate(ranks):
+            cfg.ranks[m] = int(r)
+        cfg.theta, cfg.max_iters, cfg.tol, cfg.seed = theta, max_iters, tol, seed
+        cfg.leaf_block, cfg.device = leaf_block, device
+        n = len(nodes)
+        infos = (TTNodeInfo * max(n, 1))()
+        cores = (dptr * max(n, 1))()
+        facs = (dptr * max(n * p, 1))()
+        keep = []
+        for i, v in enumerate(nodes):
+            infos[i].id, infos[i].begin, infos[i].end = v.id, v.begin, v.end
+            infos[i].kind, infos[i].left, infos[i].right = v.kind, v.left, v.right
+            f = decompositions.get(v.id) if v.has_decomposition else None
+            infos[i].has_decomposition = 1 if f is not None else 0
+            if f is None:
+                continue
+            for m in range(p):
+                infos[i].ranks[m] = f.rank(m)
+            c = np.ascontiguousarray(f.core, dtype=np.float64).ravel()
+            ms = [np.asfortranarray(f.factors[m], dtype=np.float64) for m in range(p)]
+            keep.append((c, ms))
+            cores[i] = _d(c)
+            for m in range(p):
+                facs[i * p + m] = ms[m].ctypes.data_as(dptr)
+        h = vp()
+        _check(lib().tt_tree_from_parts(C.byref(cfg), infos, n, cores, facs, root, timespan, stitch_count,
+                                         C.byref(h)))
+        self = cls.__new__(cls)
+        self._h = h
+        self.nontemporal = tuple(int(d) for d in nontemporal)
+        self.ranks = tuple(int(r) for r in ranks)
+        self.theta, self.leaf_block, self.device = theta, leaf_block, device
+        self.max_iters, self.tol, self.seed = max_iters, tol, seed
+        return self
 
 
 def brute_force_batch(x: np.ndarray, ranges, ranks: Sequence[int], max_iters: int = 20, tol: float = 0.01,

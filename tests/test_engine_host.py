@@ -37,7 +37,27 @@ def test_abi_struct_sizes_match_header():
     assert C.sizeof(E.tucktree.TTHit) == 32
     assert C.sizeof(E.tucktree.TTRange) == 16
     assert C.sizeof(E.tucktree.TTNodeInfo) == 8 * 3 + 8 + 16 + 64
-    assert C.sizeof(E.tucktree.TTQueryOut) == 8 + 64 + 64 + 8 + 8 + 8
+    assert C.sizeof(E.tucktree.TTQueryOut) == 8 + 64 + 64 + 8 + 8 + 8 + 8 + 8 + 8
+
+
+def test_abi_struct_sizes_match_compiled_header(tmp_path):
+    """The ctypes mirror and the C header agree (sizes and field offsets as the
+    C compiler lays them out)."""
+    import ctypes as C
+    import subprocess
+
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "tucktree_b200.h"\n'
+                   'int main(void){printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(tt_config), sizeof(tt_node_info),'
+                   ' sizeof(tt_hit), sizeof(tt_range), sizeof(tt_query_out), offsetof(tt_query_out, trace_cap),'
+                   ' offsetof(tt_query_out, trace)); return 0;}\n')
+    exe = tmp_path / "sz"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    got = [int(v) for v in subprocess.check_output([str(exe)]).split()]
+    T = E.tucktree
+    want = [C.sizeof(T.TTConfig), C.sizeof(T.TTNodeInfo), C.sizeof(T.TTHit), C.sizeof(T.TTRange),
+            C.sizeof(T.TTQueryOut), T.TTQueryOut.trace_cap.offset, T.TTQueryOut.trace.offset]
+    assert got == want
 
 
 def _structure_tree(nontemporal, ranks, B, T):
