@@ -382,6 +382,87 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_engine_sharded(args, rank, world, local_rank):
+    """--form burst at N > 1: the SURVEY §8(e) partitioning. Each rank builds the
+    subtree of its leaf run from its own slices (no raw data moves), the node
+    payloads are NCCL all-gathered and the top log2(N) levels stitched, then
+    the query batch is split by cost and only the small results are gathered.
+    Total work is fixed as N grows ("scaling": "strong")."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2501_06647_b200 as eng
+    from paper_2501_06647_b200 import distributed as D
+    from paper_2501_06647_b200 import shard, synth
+
+    if world == 1:  # --sharded without torchrun: a world of one
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
+    dist.init_process_group("nccl")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    w = synth.CONFIGS[args.config]
+    T = w.shape[0]
+    nq = args.queries or w.n_queries
+    B = w.leaf_block
+    T = (T // B) * B
+    plan = shard.plan_build(T // B, world)
+    lo, hi = D.run_of(plan[rank], B)
+    xd = synth.generate_torch(w, seed=0, T=T, device=dev)  # one series; each rank reads only its run
+    ranges = synth.ranges(w, T, nq, seed=1)
+    be = D.EngineBackend(w.shape[1:], w.ranks, B, device=local_rank)
+    ss = int(np.prod(w.shape[1:]))
+
+    def step():
+        tree, gs, st = D.build_sharded(be, xd.data_ptr() + 8 * lo * ss, T, plan, rank, dev, on_device=True)
+        torch.cuda.synchronize()
+        tb = time.perf_counter()
+        res, u0 = D.query_sharded(be, tree, ranges, rank, world, dev)
+        torch.cuda.synchronize()
+        return st, time.perf_counter() - tb
+
+    for _ in range(args.warmup):
+        step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = eng.kernel_launches()
+    tq = 0.0
+    with ClockSampler(local_rank) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            st, dq = step()
+            tq += dq
+        ev1.record()
+        torch.cuda.synchronize()
+    span = ev0.elapsed_time(ev1)
+    launches = eng.kernel_launches() - launches0
+    vals = torch.tensor([span, tq * 1e3], dtype=torch.float64, device=dev)
+    dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    span, tq_ms = [float(v) for v in vals.tolist()]
+    if rank == 0:
+        K = args.steps
+        line = {
+            "metric": "range_tucker_queries_per_s", "value": round(nq * K / (tq_ms / 1e3), 3), "unit": "queries/s",
+            "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": round(span / K, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded; " + w.desc + ")",
+            "config": {"workload": w.name + "_sharded", "shape": [T] + list(w.shape[1:]), "ranks": list(w.ranks),
+                       "leaf_block": B, "queries_per_step": nq, "slices_per_step": T,
+                       "parallelism": f"node-partitioned build over {world} ranks + cost-split query batch",
+                       "step": "sharded build (local subtrees, NCCL all-gather of node payloads, top stitches, "
+                               "tree install) + sharded query batch (NCCL all-gather of the small results)"},
+            "append": {"value": round(T * K / (span / 1e3), 3), "unit": "slices/s (whole step)"},
+            "build_stats": st,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 # ---------------------------------------------------------------------------
 # Streaming form (BASELINE C3): single-slice appends with interleaved queries.
 def stream_layout(w, steps_total):
@@ -746,6 +827,7 @@ def main():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--form", default="", choices=["", "stream", "burst"])
     ap.add_argument("--cpu-cycles", type=int, default=2)
+    ap.add_argument("--sharded", action="store_true", help="burst form through the sharded path even at N = 1")
     ap.add_argument("--queries", type=int, default=0)
     ap.add_argument("--cpu-queries", type=int, default=64)
     ap.add_argument("--ref-queries", type=int, default=32)
@@ -761,7 +843,12 @@ def main():
     if args.impl == "reference":
         (run_reference_stream if form == "stream" else run_reference)(args, rank, world)
     else:
-        (run_engine_stream if form == "stream" else run_engine)(args, rank, world, local_rank)
+        if form == "stream":
+            run_engine_stream(args, rank, world, local_rank)
+        elif world > 1 or args.sharded:
+            run_engine_sharded(args, rank, world, local_rank)
+        else:
+            run_engine(args, rank, world, local_rank)
 
 
 if __name__ == "__main__":

@@ -193,7 +193,8 @@ def _compare_trees(E, series, ranks, B, theta=0.7, max_iters=20, seed=20240117, 
             want = ora.range_query(ts, te)
             assert got.sweeps == len(want.objective), (ts, te)
             # AlsTrace: the per-sweep objective of the query's stitch (query.hpp:48-50)
-            np.testing.assert_allclose(got.objective, want.objective, rtol=1e-8, atol=1e-12 * max(want.objective[0], 1.0))
+            np.testing.assert_allclose(got.objective, want.objective, rtol=1e-8,
+                                       atol=1e-12 * float(np.sum(series[ts:te] ** 2)))
             assert_factors_match(series[ts:te], got, want, f"query [{ts},{te})")
     return ora, eng
 

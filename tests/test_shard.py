@@ -102,3 +102,77 @@ def test_gloo_world2_sharded_recall_and_gather():
         p.join(timeout=30)
     assert ok
     assert owners == [0, 1]
+
+
+def _dist_worker(rank, world, port, out_q):
+    """Node-partitioned build + sharded queries on gloo with the oracle as the
+    backend: every rank ends with the full set of node payloads (its subtree's
+    computed locally, the rest all-gathered, the top log2(G) levels stitched from
+    gathered children) and the gathered query results; rank 0 compares them with
+    the single-process oracle tree."""
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+    from paper_2501_06647_b200 import distributed as D
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(3)
+        T, B, nt, ranks = 16 * 4, 4, (5, 4), (3, 3, 2)
+        x = O.generate_synthetic([T, 5, 4], [3, 3, 2], 0.1, 9)
+        plan = shard.plan_build(T // B, world)
+        lo, hi = D.run_of(plan[rank], B)
+        be = D.OracleBackend(nt, ranks, B, x)
+        tree, gs, stats = D.build_sharded(be, x[lo:hi], T, plan, rank, "cpu")
+        ranges = []
+        while len(ranges) < 20:
+            a, b = sorted(int(v) for v in rng.integers(0, T + 1, size=2))
+            if a < b:
+                ranges.append((a, b))
+        res, u0 = D.query_sharded(be, tree, ranges, rank, world, "cpu")
+        ok, msgs = True, []
+        if rank == 0:
+            ref = O.Tree(nt, ranks, leaf_block=B)
+            ref.append(x)
+            _, payloads = tree
+            ok = [(v.id, v.begin, v.end, v.kind, v.left, v.right, v.has_decomposition) for v in gs.nodes] == \
+                 [(v.id, v.begin, v.end, v.kind, v.left, v.right, v.has_decomposition) for v in ref.nodes()]
+            for v in ref.nodes():
+                if v.has_decomposition:
+                    want, got = ref.node_factors(v.id), payloads[v.id]
+                    ok = ok and np.allclose(O.reconstruct(want), O.reconstruct(O.Factors(got.core, got.factors)),
+                                            atol=1e-10)
+            for qi, (ts, te) in enumerate(ranges):
+                want = ref.range_query(ts, te)
+                got = res[qi]
+                ok = ok and got.objective == [float(v) for v in want.objective] or \
+                    np.allclose(got.objective, want.objective, rtol=1e-10)
+                ok = ok and np.allclose(got.core, want.core, atol=1e-9) and \
+                    all(np.allclose(a, b, atol=1e-9) for a, b in zip(got.factors[1:], want.factors[1:]))
+                if got.factors[0] is not None:
+                    ok = ok and np.allclose(got.factors[0], want.factors[0], atol=1e-9)
+            msgs = stats
+        out_q.put((rank, bool(ok), msgs, sorted(u0)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(180)
+def test_gloo_world2_node_partitioned_build_and_queries():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dist_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=170) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=30)
+    got.sort()
+    assert got[0][1], got[0][2]
+    stats = got[0][2]
+    assert stats["top_stitches"] >= 1 and stats["gathered_nodes"] > stats["local_nodes"] > 0
+    # U_0 stayed on the producing rank: the two ranks' query sets are disjoint and cover the batch
+    assert sorted(got[0][3] + got[1][3]) == list(range(20)) and not set(got[0][3]) & set(got[1][3])
