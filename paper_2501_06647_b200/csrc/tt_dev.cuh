@@ -588,11 +588,14 @@ __device__ __noinline__ double* sym_topk_si_k(const double* __restrict__ G, int 
   bool conv = false;
   int it = 0;
   for (; it < kGramSiMaxIter; ++it) {
+    long long tp = tstart();
     for (int idx = threadIdx.x; idx < n * K; idx += blockDim.x) {
       const int i = idx % n, j = idx / n;
       W[idx] = dot4(Gp + int64_t(i) * ldp, 1, U + int64_t(j) * n, 1, n);
     }
     __syncthreads();
+    tstop_si(sc, kSiAtU, tp);
+    tp = tstart();
     gemm(K, K, n, U, n, 1, W, 1, n, B, 1, K, false, sc);  // B = U^T W
     double rsq = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -611,8 +614,10 @@ __device__ __noinline__ double* sym_topk_si_k(const double* __restrict__ G, int 
     for (int e = threadIdx.x; e < K * K; e += blockDim.x) bsq = fma(B[e], B[e], bsq);
     rsq = block_sum(rsq, sc);
     bsq = block_sum(bsq, sc);
+    tstop_si(sc, kSiAY, tp);
     if (!(bsq > 0.0)) return nullptr;
-    if (rsq <= 1e-26 * bsq) {
+    // relative residual 1e-12: the subspace error is <= 1e-12 / relative gap
+    if (rsq <= 1e-24 * bsq) {
       conv = true;
       break;
     }
@@ -623,13 +628,43 @@ __device__ __noinline__ double* sym_topk_si_k(const double* __restrict__ G, int 
       conv = true;
       break;
     }
+    // Powering: orthonormalise G^m U instead of G U. The Rayleigh quotients on
+    // B's diagonal bound the conditioning of G^m U by ratio^m; m is the largest
+    // of 1..3 keeping it <= 1e5 (CholQR2 stays exact there), so an outer
+    // iteration contracts the error by rho^m for one CholQR2.
+    {
+      if (threadIdx.x == 0) {
+        double bmax = 0.0, bmin = INFINITY;
+        for (int j = 0; j < K; ++j) {
+          bmax = fmax(bmax, B[j + j * K]);
+          bmin = fmin(bmin, B[j + j * K]);
+        }
+        const double ratio = bmin > 0.0 ? bmax / bmin : INFINITY;
+        sc.ibcast[3] = ratio <= 46.0 ? 3 : (ratio <= 316.0 ? 2 : 1);
+      }
+      __syncthreads();
+      const int extra = sc.ibcast[3] - 1;
+      for (int e = 0; e < extra; ++e) {  // U <- G W, then swap: W holds G^(1+e+1) U_old
+        for (int idx = threadIdx.x; idx < n * K; idx += blockDim.x) {
+          const int i = idx % n, j = idx / n;
+          U[idx] = dot4(Gp + int64_t(i) * ldp, 1, W + int64_t(j) * n, 1, n);
+        }
+        __syncthreads();
+        double* t = U;
+        U = W;
+        W = t;
+      }
+    }
     double* t = U;  // U <- orth(W)
     U = W;
     W = t;
+    tp = tstart();
     if (!cholqr_pass_k<K>(U, n, small, sc) || !cholqr_pass_k<K>(U, n, small, sc)) return nullptr;
+    tstop_si(sc, kSiQR, tp);
   }
   if (!conv) return nullptr;
   if (threadIdx.x == 0) sc.si_iters += it + 1;
+  const long long trr = tstart();
   double* diag = nullptr;
   const double* R = eig_run(B, K, small, order, dsm, &diag, sc);
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -647,6 +682,7 @@ __device__ __noinline__ double* sym_topk_si_k(const double* __restrict__ G, int 
   }
   if (threadIdx.x < K) lam[threadIdx.x] = diag[order[threadIdx.x] * (K + 1)];
   __syncthreads();
+  tstop_si(sc, kSiRR, trr);
   if (staged) {  // hand the result back in the caller's global buffer
     for (int idx = threadIdx.x; idx < n * K; idx += blockDim.x) Wg[idx] = W[idx];
     __syncthreads();

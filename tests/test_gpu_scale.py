@@ -1,0 +1,231 @@
+"""Parity at the BASELINE configs' own data and scale (VERDICT r1 "next" #1).
+
+* C2 at full T = 32768 (the burst bench's own series and query law): the
+  engine's tree against the oracle's, then 100 of the longest and 100 random
+  of the bench's 1000 queries.
+* C3 with its Student-t(df=3) data: T = 2048 end to end; and at the full
+  build size (12288 slices, device-generated like the streaming bench)
+  node-locally: the oracle re-decomposes sampled leaf blocks from the GPU's own
+  bytes and re-stitches sampled intermediate nodes from the GPU's own children,
+  and re-answers [0, T) from the GPU's own hit nodes.
+* C4 at full T = 8192 node-locally, plus query-local parity for sampled ranges.
+
+Floating point per the north star: |relerr_gpu - relerr_oracle| <= 1e-6 and
+sin of the largest principal angle <= 1e-6 on gapped columns; integers
+(hit sets, column counts, sweep counts) bit-exact. Each test reports its worst
+deviations as a warning line (visible in the pytest summary).
+"""
+import warnings
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2501_06647_b200 import synth
+from tests import helpers as H
+from tests.test_gpu_parity import E  # noqa: F401 (fixture)
+
+pytestmark = pytest.mark.gpu
+
+RELERR_TOL = 1e-6
+ANGLE_TOL = 1e-6
+GAP_TOL = 1e-6
+
+
+def tucker_inner(c1, f1, c2, f2):
+    """<c1 x {f1}, c2 x {f2}> without forming either tensor."""
+    acc = np.asarray(c2, dtype=np.float64)
+    for m in range(len(f1)):
+        acc = H.mode_product(acc, f1[m].T @ f2[m], m)
+    return float(np.sum(acc * c1))
+
+
+def rec_distance(a, b):
+    """||rec(a) - rec(b)|| / ||rec(b)|| in factored form."""
+    aa = tucker_inner(a.core, a.factors, a.core, a.factors)
+    bb = tucker_inner(b.core, b.factors, b.core, b.factors)
+    ab = tucker_inner(a.core, a.factors, b.core, b.factors)
+    return float(np.sqrt(max(aa + bb - 2 * ab, 0.0) / max(bb, 1e-300)))
+
+
+def relerr_factored(x, f):
+    """||x - rec(f)|| / ||x|| through the projection x x_m U_m^T (x never reconstructed)."""
+    proj = x
+    for m, u in enumerate(f.factors):
+        proj = H.mode_product(proj, u.T, m)
+    xx = float(np.sum(x * x))
+    ff = tucker_inner(f.core, f.factors, f.core, f.factors)
+    xf = float(np.sum(proj * f.core))
+    return float(np.sqrt(max(xx - 2 * xf + ff, 0.0) / xx))
+
+
+def gapped_sin(got, want):
+    """Largest sin angle over modes whose kept columns are separated by a gap,
+    judged on the oracle's core spectrum of that mode."""
+    worst = 0.0
+    for m in range(want.order):
+        s = np.linalg.svd(H.unfold(want.core, m), compute_uv=False)
+        k = got.rank(m)
+        if s.size == 0 or s[0] == 0:
+            continue
+        if k < len(s) and (s[k - 1] - s[k]) / s[0] < GAP_TOL:
+            continue
+        worst = max(worst, H.max_sin_angle(got.factors[m], want.factors[m]))
+    return worst
+
+
+class Worst:
+    def __init__(self, tag):
+        self.tag, self.drel, self.sin, self.rec, self.n = tag, 0.0, 0.0, 0.0, 0
+
+    def add(self, got, want, x=None, where=""):
+        assert [got.rank(m) for m in range(got.order)] == [want.rank(m) for m in range(want.order)], where
+        self.n += 1
+        d = rec_distance(got, want)
+        self.rec = max(self.rec, d)
+        assert d <= 1e-6, (where, d)
+        a = gapped_sin(got, want)
+        self.sin = max(self.sin, a)
+        assert a <= ANGLE_TOL, (where, a)
+        if x is not None:
+            dr = abs(relerr_factored(x, got) - relerr_factored(x, want))
+            self.drel = max(self.drel, dr)
+            assert dr <= RELERR_TOL, (where, dr)
+
+    def report(self):
+        warnings.warn(f"[parity {self.tag}] {self.n} comparisons: worst |relerr_gpu - relerr_oracle| = "
+                      f"{self.drel:.2e}, worst sin angle = {self.sin:.2e}, worst rec distance = {self.rec:.2e}")
+
+
+def _same_structure(eng, ora):
+    assert eng.timespan() == ora.timespan and eng.stitch_count() == ora.stitch_count
+    assert [(v.id, v.begin, v.end, v.kind, v.left, v.right) for v in eng.nodes()] == \
+           [(v.id, v.begin, v.end, v.kind, v.left, v.right) for v in ora.nodes()]
+
+
+# ---------------------------------------------------------------------------- C2
+@pytest.mark.timeout(1800)
+def test_c2_full_scale_bench_queries(E):
+    w = synth.CONFIGS["c2"]
+    T = w.shape[0]
+    x = synth.generate(w, seed=0)  # the burst bench's series
+    eng = E.StreamSegmentTree(w.shape[1:], w.ranks, leaf_block=w.leaf_block)
+    ora = O.Tree(w.shape[1:], w.ranks, leaf_block=w.leaf_block)
+    eng.append(x)
+    ora.append(x)
+    _same_structure(eng, ora)
+    ranges = synth.ranges(w, T, w.n_queries, seed=1)  # the bench's 1000 queries
+    lens = ranges[:, 1] - ranges[:, 0]
+    longest = np.argsort(-lens, kind="stable")[:100]
+    rnd = np.random.default_rng(7).choice(np.setdiff1d(np.arange(len(ranges)), longest), 100, replace=False)
+    sel = [tuple(int(v) for v in ranges[i]) for i in np.concatenate([longest, rnd])]
+    got = eng.range_query_batch(sel, return_info=True)
+    wst = Worst("C2 T=32768, 200 bench queries")
+    for qi, ((ts, te), (g, nh)) in enumerate(zip(sel, got)):
+        hits = ora.recall(ts, te)
+        assert [(h.node, h.begin, h.end, h.flag) for h in eng.recall(ts, te)] == hits and nh == len(hits)
+        want = ora.range_query(ts, te)
+        assert g.sweeps == len(want.objective), (ts, te)
+        wst.add(g, want, x[ts:te] if qi % 10 == 0 else None, f"[{ts},{te})")
+    wst.report()
+
+
+# ---------------------------------------------------------------------------- C3
+@pytest.mark.timeout(1800)
+def test_c3_student_t_end_to_end(E):
+    w = synth.CONFIGS["c3"]
+    T = 2048
+    x = synth.generate(w, seed=0, T=T)
+    eng = E.StreamSegmentTree(w.shape[1:], w.ranks, leaf_block=w.leaf_block)
+    ora = O.Tree(w.shape[1:], w.ranks, leaf_block=w.leaf_block)
+    eng.append(x[:T - 40])  # burst (batched leaves), then single-slice appends (cluster leaf kernel)
+    for t in range(T - 40, T):
+        eng.append(x[t])
+    ora.append(x)
+    _same_structure(eng, ora)
+    wst = Worst("C3 Student-t T=2048")
+    for v in ora.nodes():
+        if v.has_decomposition and (v.kind == 1 or v.id % 5 == 0):
+            wst.add(eng.decomposition(v.id), ora.node_factors(v.id), x[v.begin:v.end], f"node {v.id}")
+    rng = np.random.default_rng(3)
+    qs = [(0, T), (0, T - 17), (5, 1500)] + [tuple(sorted(int(a) for a in rng.choice(T + 1, 2, replace=False)))
+                                            for _ in range(12)]
+    for (ts, te), g in zip(qs, eng.range_query_batch(qs)):
+        want = ora.range_query(ts, te)
+        assert g.sweeps == len(want.objective)
+        wst.add(g, want, x[ts:te], f"[{ts},{te})")
+    wst.report()
+
+
+def _node_local(E, eng, xd, w, wst, leaf_ids, stitch_ids):
+    B = w.leaf_block
+    for nid in leaf_ids:
+        v = eng.node(nid)
+        blk = xd[v.begin:v.end].cpu().numpy()
+        wst.add(eng.decomposition(nid), O.tucker_als(blk, w.ranks), blk, f"leaf {nid}")
+    for nid in stitch_ids:
+        v = eng.node(nid)
+        kids = [eng.decomposition(v.left), eng.decomposition(v.right)]
+        parts = [O.Factors(k.core, k.factors) for k in kids]
+        want = O.stitch(parts, w.ranks)
+        wst.add(eng.decomposition(nid), want, None, f"stitch {nid} [{v.begin},{v.end})")
+    del B
+
+
+def _query_local(E, eng, xd, w, wst, qs):
+    """The oracle re-answers each query from the GPU's own hit nodes
+    (query.cpp:49-69: entire = stored, partial = QR-trimmed, tail = ALS of raw)."""
+    got = eng.range_query_batch(qs)
+    for (ts, te), g in zip(qs, got):
+        parts = []
+        for h in eng.recall(ts, te):
+            if h.flag == 2:
+                parts.append(O.tucker_als(xd[h.begin:h.end].cpu().numpy(), w.ranks))
+                continue
+            v = eng.node(h.node)
+            f = eng.decomposition(h.node)
+            f = O.Factors(f.core, f.factors)
+            parts.append(f if h.flag == 0 else O.partial_hit_factors(f, h.begin - v.begin, h.end - v.begin))
+        want = O.stitch(parts, w.ranks)
+        assert g.sweeps == len(want.objective), (ts, te)
+        wst.add(g, want, None, f"query [{ts},{te})")
+
+
+@pytest.mark.timeout(1800)
+def test_c3_full_build_node_local(E):
+    import torch
+
+    w = synth.CONFIGS["c3"]
+    T0 = w.build_T
+    xd = synth.generate_torch(w, seed=0, device="cuda")
+    eng = E.StreamSegmentTree(w.shape[1:], w.ranks, leaf_block=w.leaf_block)
+    eng.append_device(xd.data_ptr(), T0)
+    for t in range(T0, T0 + 37):  # a raw tail through single-slice appends
+        eng.append_device(xd.data_ptr() + 8 * t * int(np.prod(w.shape[1:])), 1)
+    torch.cuda.synchronize()
+    nodes = eng.nodes()
+    leaves = [v.id for v in nodes if v.kind == 0]
+    inter = sorted([v for v in nodes if v.kind == 1], key=lambda v: v.end - v.begin)
+    stitch_ids = [inter[0].id, inter[len(inter) // 2].id, inter[-2].id, inter[-1].id]
+    wst = Worst("C3 full build (12288 + 37 slices) node-local")
+    _node_local(E, eng, xd, w, wst, [leaves[0], leaves[77], leaves[-1]], stitch_ids)
+    _query_local(E, eng, xd, w, wst, [(0, T0 + 37), (100, 9000), (4000, T0)])
+    wst.report()
+
+
+# ---------------------------------------------------------------------------- C4
+@pytest.mark.timeout(1800)
+def test_c4_full_scale_node_and_query_local(E):
+    w = synth.CONFIGS["c4"]
+    T = w.shape[0]
+    xd = synth.generate_torch(w, seed=0, device="cuda")
+    eng = E.StreamSegmentTree(w.shape[1:], w.ranks, leaf_block=w.leaf_block)
+    eng.append_device(xd.data_ptr(), T)
+    nodes = eng.nodes()
+    leaves = [v.id for v in nodes if v.kind == 0]
+    inter = sorted([v for v in nodes if v.kind == 1], key=lambda v: v.end - v.begin)
+    wst = Worst("C4 T=8192 node/query-local")
+    _node_local(E, eng, xd, w, wst, [leaves[0], leaves[-1]], [inter[0].id, inter[-3].id, inter[-1].id])
+    rq = synth.ranges(w, T, 8, seed=1)
+    _query_local(E, eng, xd, w, wst, [tuple(int(v) for v in r) for r in rq])
+    wst.report()
