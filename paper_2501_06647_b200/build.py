@@ -14,8 +14,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libtucktree_b200.so")
-SOURCES = ["tt_leaf.cu", "tt_wide.cu", "tt_stitch.cu", "tt_host.cpp"]
-HEADERS = ["tt_common.h", "tt_block.cuh", "tt_dev.cuh"]
+SOURCES = ["tt_leaf.cu", "tt_wide.cu", "tt_stitch.cu", "tt_stitch_wide.cu", "tt_host.cpp"]
+HEADERS = ["tt_common.h", "tt_block.cuh", "tt_dev.cuh", "tt_stitch_body.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -170,7 +170,7 @@ TT_HD LeafWs leaf_ws_layout(int p, int64_t len, const int64_t* d, const int64_t*
 }
 
 struct StitchWs {
-  int64_t P, C, S, E, A, G, V, T1, T2, TB1, TB2, Z, WK, HH, SI, misc, total, gram_n;
+  int64_t P, C, S, E, A, G, V, T1, T2, TB1, TB2, Z, WK, HH, SI, misc, xch, gpart, total, gram_n;
   int64_t chain;  // per-part stride of the part-batched mode-product chains (TB1/TB2)
   int64_t per_part_P, per_part_C, per_part_S, per_part_E;
 };
@@ -178,8 +178,9 @@ struct StitchWs {
 // rcx[m] = max(rc[m], max_i rho_im): bound on every intermediate extent. The C, E
 // and A regions hold the parts' stacked temporal rows (R = sum rho_i0 <=
 // nparts*rcx0 rows; C row-major R x Q, E and A column-major R x k0, ld R).
+// cs > 0: the cluster stitch kernel's exchange slots and per-CTA partial Grams.
 TT_HD StitchWs stitch_ws_layout(int p, int64_t L, const int64_t* d, const int64_t* req, const int64_t* rho_max,
-                                int nparts) {
+                                int nparts, int64_t cs = 0) {
   int64_t dd[kMaxP], rc[kMaxP], rcx[kMaxP];
   dd[0] = L;
   for (int m = 1; m < p; ++m) dd[m] = d[m];
@@ -220,7 +221,9 @@ TT_HD StitchWs stitch_ws_layout(int p, int64_t L, const int64_t* d, const int64_
   for (int m = 0; m < p; ++m) kmax = imax(kmax, rc[m]);
   w.SI = w.HH + rcx[0] * rcx[0];
   w.misc = w.SI + si_size(maxrows, g, kmax);
-  w.total = w.misc + kMisc + 4 * g;
+  w.xch = w.misc + kMisc + 4 * g;
+  w.gpart = w.xch + kXch;
+  w.total = w.gpart + cs * g * g;
   w.total = (w.total + 31) & ~int64_t(31);
   return w;
 }

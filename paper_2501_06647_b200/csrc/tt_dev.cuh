@@ -833,6 +833,78 @@ static __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows,
   tstop(sc, kPhOrtho, ts);
 }
 
+// ---------------------------------------------------------------------------
+// Thread-block clusters (the cluster kernels of tt_wide.cu and tt_stitch.cu)
+__device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cl_size() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cl_id() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// leading_left_singular_vectors (linalg.cpp:45-64) of the mode unfolding of a
+// row-major (outer, rows, inner) tensor for the cluster: when llsv_unfold
+// takes its Gram route with a tiled Gram, every CTA forms the Gram over its
+// share of the long side into its partial slot, and the leader sums the
+// partials in rank order and runs the solver; otherwise the leader does it
+// all. Called by every CTA of the cluster (one cluster barrier inside on the
+// distributed route); U is valid on the leader afterwards.
+static __device__ void wide_llsv(const double* P, int64_t outer, int64_t rows, int64_t inner, int64_t k, double* U,
+                          double* G, double* V, double* misc, double* dsm, BlockScratch& sc, int64_t kprev,
+                          double* si, double* gpart, int rank, int CS) {
+  const int64_t cols = outer * inner;
+  const bool wide = rows <= cols;
+  const int n = int(wide ? rows : cols);
+  const bool dist = CS > 1 && !llsv_uses_subspace(rows, cols, k, kprev, si, sc) && n >= kGramTiledMinN &&
+                    n * 4 <= sc.dsm_cap;
+  if (!dist) {
+    if (rank == 0) llsv_unfold(P, outer, rows, inner, k, U, G, V, misc, dsm, sc, kprev, si);
+    return;
+  }
+  const long long tg = tstart();
+  const int64_t nx = wide ? cols : rows;
+  const int64_t per = (nx + CS - 1) / CS;
+  const int64_t x0 = imin(nx, int64_t(rank) * per), x1 = imin(nx, x0 + per);
+  double* Gp = gpart + int64_t(rank) * n * n;
+  auto unf = [&](int64_t i, int64_t c) {
+    const int64_t o = c / inner, t = c - o * inner;
+    return P[(o * rows + i) * inner + t];
+  };
+  if (x1 <= x0) {
+    for (int64_t idx = threadIdx.x; idx < int64_t(n) * n; idx += blockDim.x) Gp[idx] = 0.0;
+    __syncthreads();
+  } else if (wide) {  // G = A A^T: x over the columns
+    gram_tiled(n, x1 - x0, [&](int64_t c, int a) { return unf(a, x0 + c); }, true, Gp, dsm, sc.dsm_cap);
+  } else {  // G = A^T A: x over the rows
+    gram_tiled(n, x1 - x0, [&](int64_t i, int a) { return unf(x0 + i, a); }, false, Gp, dsm, sc.dsm_cap);
+  }
+  cl_sync();
+  if (rank == 0) {
+    for (int64_t idx = threadIdx.x; idx < int64_t(n) * n; idx += blockDim.x) {
+      double v = 0.0;
+      for (int r = 0; r < CS; ++r) v += gpart[int64_t(r) * n * n + idx];
+      G[idx] = v;
+    }
+    __syncthreads();
+    tstop(sc, kPhGram, tg);
+    llsv_unfold(P, outer, rows, inner, k, U, G, V, misc, dsm, sc, kprev, si, /*gram_ready=*/true);
+  }
+}
+
+
 extern std::atomic<int64_t> g_launches;
 
 // Sets a kernel's dynamic shared-memory cap on the current device, once per

@@ -34,6 +34,9 @@ cudaError_t launch_leaf(const Params& prm, const LeafDesc* d_descs, int n, cudaS
 cudaError_t launch_stitch(const Params& prm, const StitchDesc* d_descs, const StitchPart* d_parts, int n,
                           cudaStream_t st);
 int leaf_wide_cluster();
+int stitch_wide_cluster();
+cudaError_t launch_stitch_wide(const Params& prm, const StitchDesc* d_descs, const StitchPart* d_parts, int n, int cs,
+                               cudaStream_t st);
 cudaError_t launch_leaf_wide(const Params& prm, const LeafDesc* d_descs, int n, int cs, cudaStream_t st);
 cudaError_t launch_copy_segments(const CopySeg* d_segs, int n, cudaStream_t st);
 cudaError_t launch_partial_hit(const double* V0, int64_t ld, int64_t b, int64_t len, int n, const double* core,
@@ -449,6 +452,23 @@ std::vector<ProblemStatus> run_stitch_batch(Exec& ex, const Params& prm, std::ve
     wsz[i] = ws_sizes[perm[i]];
   }
   std::vector<ProblemStatus> st(static_cast<size_t>(n));
+  // Few problems (streamed appends, single queries): one thread-block cluster
+  // per problem (stitch_wide_kernel); TT_WIDE=0/1 forces either path.
+  const int cs = stitch_wide_cluster();
+  bool wide = cs > 0;
+  if (wide) {
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ex.device);
+    wide = n <= std::max(1, nsm / cs);
+    if (const char* e = std::getenv("TT_WIDE")) wide = e[0] == '1';
+  }
+  if (wide)  // + exchange slots and per-CTA partial Grams
+    for (int i = 0; i < n; ++i) {
+      Index rho_max[kMaxP] = {};
+      for (int j = 0; j < descs[i].nparts; ++j)
+        for (int m = 0; m < prm.p; ++m) rho_max[m] = std::max(rho_max[m], parts[size_t(descs[i].part0) + j].rho[m]);
+      wsz[i] = stitch_ws_layout(prm.p, descs[i].L, prm.d, prm.req, rho_max, descs[i].nparts, cs).total;
+    }
   const std::vector<Index>& ws_sizes_p = wsz;
   size_t ws_total = 0;
   for (Index w : ws_sizes_p) ws_total += static_cast<size_t>(w);
@@ -469,8 +489,12 @@ std::vector<ProblemStatus> run_stitch_batch(Exec& ex, const Params& prm, std::ve
   cuda_check(cudaMemcpyAsync(ex.d_parts.p, parts.data(), sizeof(StitchPart) * parts.size(), cudaMemcpyHostToDevice,
                              ex.stream),
              "upload stitch parts");
-  cuda_check(launch_stitch(prm, ex.d_desc.as<StitchDesc>(), ex.d_parts.as<StitchPart>(), n, ex.stream),
-             "stitch_als_kernel launch");
+  if (wide)
+    cuda_check(launch_stitch_wide(prm, ex.d_desc.as<StitchDesc>(), ex.d_parts.as<StitchPart>(), n, cs, ex.stream),
+               "stitch_wide_kernel launch");
+  else
+    cuda_check(launch_stitch(prm, ex.d_desc.as<StitchDesc>(), ex.d_parts.as<StitchPart>(), n, ex.stream),
+               "stitch_als_kernel launch");
   std::vector<int32_t> hs(size_t(n) * kStatusInts);
   std::vector<double> ho(size_t(n) * prm.max_iters);
   cuda_check(cudaMemcpyAsync(hs.data(), ex.d_status.p, hs.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, ex.stream),
