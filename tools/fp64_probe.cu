@@ -45,6 +45,24 @@ __global__ void __launch_bounds__(256) tput_kernel(double* out, int iters) {
   if (s == 12345.678) out[0] = s;
 }
 
+// FP64 tensor-core (DMMA) throughput: mma.sync.aligned.m8n8k4 f64, 8
+// independent accumulator fragments per warp (2 flops x 8x8x4 per mma).
+__global__ void __launch_bounds__(256) dmma_kernel(double* out, int iters) {
+  double acc[8][2];
+  for (int k = 0; k < 8; ++k) acc[k][0] = acc[k][1] = threadIdx.x * 1e-3 + k;
+  const double a = 0.999999 + threadIdx.x * 1e-9, b = 1e-7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                   : "+d"(acc[k][0]), "+d"(acc[k][1])
+                   : "d"(a), "d"(b));
+  }
+  double s = 0;
+  for (int k = 0; k < 8; ++k) s += acc[k][0] + acc[k][1];
+  if (s == 12345.678) out[0] = s;
+}
+
 int main() {
   double* d;
   long long* c;
@@ -72,5 +90,20 @@ int main() {
   cudaEventElapsedTime(&ms, e0, e1);
   const double flops = 2.0 * 8 * iters * double(blocks) * 256;
   printf("DFMA throughput %.2f TFLOP/s (%d SMs, %.3f ms)\n", flops / ms / 1e9, nsm, ms);
+  {
+    const int dit = 4096;
+    dmma_kernel<<<nsm * 8, 256>>>(d, 16);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    dmma_kernel<<<nsm * 8, 256>>>(d, dit);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double flops = double(nsm) * 8 * (256 / 32) * dit * 8 * (2.0 * 8 * 8 * 4);
+    printf("DMMA (mma.sync m8n8k4 f64) throughput %.2f TFLOP/s (%d SMs, %.3f ms)\n", flops / (ms * 1e-3) / 1e12, nsm, ms);
+  }
   return 0;
 }
