@@ -555,24 +555,30 @@ static __device__ bool llsv_subspace(const double* P, int64_t outer, int64_t row
 // An iteration costs O(n^2 k), against O(n^3) per sweep for the Jacobi
 // fallback, so slowly converging (small-gap) problems get more iterations.
 constexpr int kGramSiMaxIter = 100;
+constexpr int kGramSiMaxK = 32;  // top-k Gram iteration: k <= 32 (BASELINE C5's ranks 20)
+// shared-memory carve-up of sym_topk_si_k: [0, 3K^2) Rayleigh-Ritz eigensolver
+// scratch, then CholeskyQR scratch (3K^2), B (K^2), then the staged G, U, W
+__host__ __device__ constexpr int topk_small_off(int K) { return K <= 16 ? 768 : 3 * K * K; }
+__host__ __device__ constexpr int topk_b_off(int K) { return K <= 16 ? 1536 : 6 * K * K; }
+__host__ __device__ constexpr int topk_stage_off(int K) { return K <= 16 ? 2048 : 7 * K * K; }
 template <int K>
 __device__ __noinline__ double* sym_topk_si_k(const double* __restrict__ G, int n, double* U, double* W,
                                               double* lam, int* order, double* dsm, BlockScratch& sc) {
-  double* small = dsm + 768;  // CholeskyQR scratch (3 K^2); dsm[0, 768) is the Rayleigh-Ritz eigensolver's
-  double* B = dsm + 1536;     // K x K
+  double* small = dsm + topk_small_off(K);  // CholeskyQR scratch (3 K^2); dsm[0, 3K^2) is the Rayleigh-Ritz eigensolver's
+  double* B = dsm + topk_b_off(K);          // K x K
   // With room, G (odd leading dimension: conflict-free row reads), U and W live
   // in shared memory for the whole iteration: every product is then an SMEM
   // stream instead of an L2-latency-bound dot product (the cluster leaf
   // kernel's 176 KB and the stitch kernel's small-batch launches have room for
   // n = 100).
   const int ldg = n | 1;
-  const bool staged = 2048 + ldg * n + 2 * n * K <= sc.dsm_cap;
+  const bool staged = topk_stage_off(K) + ldg * n + 2 * n * K <= sc.dsm_cap;
   double* const Ug = U;
   double* const Wg = W;
   const double* Gp = G;
   int ldp = n;
   if (staged) {
-    double* Gs = dsm + 2048;
+    double* Gs = dsm + topk_stage_off(K);
     for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
       const int i = idx % n, j = idx / n;
       Gs[i + j * ldg] = G[idx];
@@ -699,6 +705,8 @@ static __device__ double* sym_topk_si(const double* G, int n, int k, double* U, 
     return sym_topk_si_k<N>(G, n, U, W, lam, order, dsm, sc);
     TT_CASE(1) TT_CASE(2) TT_CASE(3) TT_CASE(4) TT_CASE(5) TT_CASE(6) TT_CASE(7) TT_CASE(8)
     TT_CASE(9) TT_CASE(10) TT_CASE(11) TT_CASE(12) TT_CASE(13) TT_CASE(14) TT_CASE(15) TT_CASE(16)
+    TT_CASE(17) TT_CASE(18) TT_CASE(19) TT_CASE(20) TT_CASE(21) TT_CASE(22) TT_CASE(23) TT_CASE(24)
+    TT_CASE(25) TT_CASE(26) TT_CASE(27) TT_CASE(28) TT_CASE(29) TT_CASE(30) TT_CASE(31) TT_CASE(32)
 #undef TT_CASE
     default:
       return nullptr;
@@ -765,7 +773,7 @@ static __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows,
   tstop(sc, kPhGram, tg);
   // eigenvectors: column c at vcol(c), eigenvalue lamc(c), descending
   const double* Vsi = nullptr;
-  if (kprev > 0 && k <= kSiMaxK && n > kGramSiMinN && n >= 2 * k && 1792 <= sc.dsm_cap) {
+  if (kprev > 0 && k <= kGramSiMaxK && n > kGramSiMinN && n >= 2 * k && 7 * k * k + 256 <= sc.dsm_cap) {
     const long long t0 = tstart();
     double* Us = V;
     double* Ws = V + int64_t(n) * k;

@@ -463,6 +463,7 @@ __device__ __forceinline__ void stitch_body(const Params& prm, const StitchDesc*
     if (leader) gemm_batched(s * (p - 1), [&](int e) { return pm_entry(e / (p - 1), 1 + e % (p - 1)); }, sc);
     const double norm = sqrt(norm_sq);
     double prev_fit = nan("");
+    bool wk_valid = false;  // wk holds the previous sweep's G0 eigenvectors (mode-0 fallback warm start)
     for (int sweep = 0; sweep < prm.max_iters; ++sweep) {
       // ================= mode 0 (stitch_temporal_unfolding, stitch.cpp:49-73)
       const int64_t k0n = stitch_mode_rank(p, d, rc, k, 0);
@@ -782,12 +783,54 @@ __device__ __forceinline__ void stitch_body(const Params& prm, const StitchDesc*
         {
           int* order = reinterpret_cast<int*>(misc);
           double* sig = misc + kMisc / 2;
+          double* lamv = misc + kMisc / 2 + 512;
           double* diag = nullptr;
           if (threadIdx.x == 0) sc.ibcast[1] = 0;
-          const double* Vp = eig_run(G, int(Q), Vg, order, dsm, &diag, sc);
+          // ranks beyond the E-coordinate iteration (C5: k0 = 20 on a 400 x 400
+          // G0): warm-started top-k Gram iteration instead of a full Jacobi of G0
+          // — start from the previous sweep's eigenvectors (wk, same directions),
+          // or in sweep 0 from the canonical vectors of G0's k0 largest diagonal
+          // entries; the Jacobi path remains the fallback
+          const double* Vsi = nullptr;
+          if (k0n > kSiMaxK && k0n <= kGramSiMaxK && Q >= 2 * k0n && Q > kGramSiMinN &&
+              7 * k0n * k0n + 256 <= sc.dsm_cap) {
+            double* Us = Vg;
+            double* Ws = Vg + Q * k0n;
+            if (wk_valid) {
+              for (int64_t idx = threadIdx.x; idx < Q * k0n; idx += blockDim.x) Us[idx] = wk[idx];
+            } else {
+              int* pick = reinterpret_cast<int*>(misc);
+              for (int q = threadIdx.x; q < int(Q); q += blockDim.x) {
+                int rank = 0;
+                const double gq = G[q + q * Q];
+                for (int l = 0; l < int(Q); ++l) {
+                  const double gl = G[l + l * Q];
+                  rank += (gl > gq || (gl == gq && l < q));
+                }
+                if (rank < k0n) pick[rank] = q;
+              }
+              __syncthreads();
+              for (int64_t idx = threadIdx.x; idx < Q * k0n; idx += blockDim.x) {
+                const int64_t j = idx % Q, c = idx / Q;
+                Us[idx] = (j == pick[c]) ? 1.0 : 0.0;
+              }
+            }
+            __syncthreads();
+            Vsi = sym_topk_si(G, int(Q), int(k0n), Us, Ws, lamv, order, dsm, sc);
+            if (threadIdx.x == 0) {
+              if (Vsi)
+                sc.si_ok += 1;
+              else
+                sc.si_fail += 1;
+            }
+          }
+          const double* Vp = Vsi;
+          if (!Vsi) Vp = eig_run(G, int(Q), Vg, order, dsm, &diag, sc);
+          auto vcol = [&](int64_t c) { return Vsi ? Vsi + c * Q : Vp + int64_t(order[c]) * Q; };
+          auto lamc = [&](int64_t c) { return Vsi ? lamv[c] : diag[order[c] * (Q + 1)]; };
           if (threadIdx.x < k0n) {
-            const double l0 = fmax(diag[order[0] * (Q + 1)], 0.0);
-            const double lc = fmax(diag[order[threadIdx.x] * (Q + 1)], 0.0);
+            const double l0 = fmax(lamc(0), 0.0);
+            const double lc = fmax(lamc(threadIdx.x), 0.0);
             const bool ok = gram_sigma_ok(lc, l0);
             sig[threadIdx.x] = ok ? 1.0 / sqrt(lc) : 0.0;
             if (!ok) atomicOr(&sc.ibcast[1], 1);
@@ -795,10 +838,11 @@ __device__ __forceinline__ void stitch_body(const Params& prm, const StitchDesc*
           __syncthreads();
           for (int64_t idx = threadIdx.x; idx < Q * k0n; idx += blockDim.x) {
             const int64_t j = idx % Q, c = idx / Q;
-            wk[idx] = Vp[j + int64_t(order[c]) * Q] * sig[c];
+            wk[idx] = vcol(c)[j] * sig[c];
           }
           __syncthreads();
           any_zero_sigma = sc.ibcast[1];
+          wk_valid = !any_zero_sigma;
         }
         // E = C W Sigma^-1 (R x k0, stacked);  A_i = S_i E_i = (U0[rows_i]^T V_i0)^T
         tgemm(R, k0n, Q, Cst, Q, 1, wk, 1, Q, Est, 1, R, false, sc);

@@ -34,6 +34,11 @@ CONFIGS = {
                    build_T=12288),
     "c4": Workload("c4", (8192, 64, 64, 8), (8, 8, 8, 4), 64, 10000,
                    "low-rank (8,8,8,4) + N(0, 0.05^2) noise; 10000 uniform ranges"),
+    # 137 GB at full T: generated on the device (generate_torch); the host
+    # generator is for reduced-T parity cases only
+    "c5": Workload("c5", (65536, 1024, 256), (20, 20, 20), 256, 50000,
+                   "low-rank (20,20,20) Gaussian core x orthonormal factors + 1% relative Gaussian noise; "
+                   "build 57344, burst-append 8192, 50000 uniform ranges", build_T=57344),
 }
 
 
@@ -71,6 +76,9 @@ def generate(w: Workload, seed: int = 0, T: int | None = None) -> np.ndarray:
         x += rng.standard_t(3, size=shape) * (np.linalg.norm(x) / np.sqrt(x.size)) * 0.3
     elif w.name == "c4":
         x += 0.05 * rng.standard_normal(shape)
+    elif w.name == "c5":
+        e = rng.standard_normal(shape)
+        x += 0.01 * np.linalg.norm(x) / np.linalg.norm(e) * e
     return x
 
 
@@ -149,4 +157,6 @@ def generate_torch(w: Workload, seed: int = 0, T: int | None = None, device="cud
             blk += st * (nrm / np.sqrt(N) * 0.3)
         elif w.name == "c4":
             blk += 0.05 * torch.randn(blk.shape, **kw)
+        elif w.name == "c5":
+            blk += (0.01 * nrm / np.sqrt(N)) * torch.randn(blk.shape, **kw)
     return x

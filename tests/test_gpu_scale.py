@@ -27,6 +27,14 @@ from tests.test_gpu_parity import E  # noqa: F401 (fixture)
 
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(autouse=True, scope="module")
+def _single_thread_oracle():
+    """The oracle's BLAS on one thread: bit-reproducible reductions, so a
+    borderline |d fit| < tol decision cannot flip between runs."""
+    O.set_threads(1)
+    yield
+
 RELERR_TOL = 1e-6
 ANGLE_TOL = 1e-6
 GAP_TOL = 1e-6
@@ -241,3 +249,32 @@ def test_c4_full_scale_node_and_query_local(E):
     rq = synth.ranges(w, T, 8, seed=1)
     _query_local(E, eng, xd, w, wst, [tuple(int(v) for v in r) for r in rq])
     wst.report()
+
+
+# ---------------------------------------------------------------------------- C5
+@pytest.mark.timeout(2400)
+def test_c5_shaped_nodes(E):
+    """C5's shape and ranks (1024 x 256 non-temporal, rank 20 > the 16-column
+    register-tiled iterations, leaf 256) at reduced T = 1024: four 512 MiB leaf
+    blocks on the cluster leaf kernel, node-local leaves and stitches, and
+    query-local ranges (the full 137 GB series does not fit one GPU's build)."""
+    import torch
+
+    w = synth.CONFIGS["c5"]
+    T = 1024
+    xd = synth.generate_torch(w, seed=0, T=T, device="cuda")
+    eng = E.StreamSegmentTree(w.shape[1:], w.ranks, leaf_block=w.leaf_block)
+    eng.append_device(xd.data_ptr(), T)
+    torch.cuda.synchronize()
+    assert eng.validate() == [] and eng.stitch_count() == 3
+    nodes = eng.nodes()
+    leaves = [v.id for v in nodes if v.kind == 0]
+    inter = sorted([v for v in nodes if v.kind == 1], key=lambda v: v.end - v.begin)
+    O.set_threads(8)  # 512 MiB blocks: let the oracle's BLAS use the host cores
+    try:
+        wst = Worst("C5-shaped (1024x256, rank 20, leaf 256, T=1024) node/query-local")
+        _node_local(E, eng, xd, w, wst, [leaves[0], leaves[-1]], [inter[0].id, inter[-1].id])
+        _query_local(E, eng, xd, w, wst, [(0, T), (100, 900), (300, 301)])
+        wst.report()
+    finally:
+        O.set_threads(1)
