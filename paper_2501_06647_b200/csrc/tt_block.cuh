@@ -322,9 +322,98 @@ __device__ __forceinline__ void gram_rows(const double* __restrict__ P, int64_t 
 // 4x4 block of the upper triangle in registers: per staged row, 8 shared loads
 // feed 16 FMAs, against 2 uncoalesced global loads per FMA for a
 // thread-per-entry Gram. Blocks beyond one per thread take further passes.
+// FP64 tensor-core (DMMA) accumulate: c += a b over one m8n8k4 fragment.
+__device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Gram on the FP64 tensor cores: G (n x n, col-major) = sum_x T(x, :)^T T(x, :),
+// T(x, a) = elem(x, a). Chunks of x are staged in shared memory as for
+// gram_tiled; each warp owns up to kTpw 8x8 tiles of the upper triangle and
+// accumulates them with mma.sync.m8n8k4.f64 over groups of 4 staged rows: lane
+// (g, q) = (lane / 4, lane % 4) feeds A(g, q) = T(x0 + q, i0 + g) and
+// B(q, g) = T(x0 + q, j0 + g) and receives G(i0 + g, j0 + 2q + {0, 1}). One
+// DMMA replaces 8 per-thread FMAs and the register tiles' shared-memory reloads.
+template <class Elem>
+__device__ __forceinline__ void gram_tiled_mma(int n, int64_t nx, Elem elem, bool x_fast, double* __restrict__ G,
+                                               double* stage, int stage_cap) {
+  constexpr int kTpw = 12;
+  const int nb = (n + 7) / 8;
+  const int ntiles = nb * (nb + 1) / 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = int(blockDim.x >> 5);
+  const int g = lane >> 2, q = lane & 3;
+  const int ch = int(imax(4, imin((nx + 3) / 4 * 4, (stage_cap / n) / 4 * 4)));
+  for (int base = 0; base < ntiles; base += nw * kTpw) {  // tile groups: each warp takes kTpw tiles
+    int ti[kTpw], tj[kTpw];
+    double acc[kTpw][2];
+#pragma unroll
+    for (int u = 0; u < kTpw; ++u) {
+      int e = base + warp * kTpw + u, bi = 0;
+      if (e >= ntiles) e = -1;
+      if (e >= 0) {
+        while (e >= nb - bi) {
+          e -= nb - bi;
+          ++bi;
+        }
+      }
+      ti[u] = e >= 0 ? 8 * bi : -1;
+      tj[u] = e >= 0 ? 8 * (bi + e) : -1;
+      acc[u][0] = acc[u][1] = 0.0;
+    }
+    for (int64_t x0 = 0; x0 < nx; x0 += ch) {
+      const int cx = int(imin(ch, nx - x0));
+      const int cx4 = (cx + 3) & ~3;
+      __syncthreads();
+      if (x_fast) {
+        for (int idx = threadIdx.x; idx < cx4 * n; idx += blockDim.x) {
+          const int x = idx % cx4, a = idx / cx4;
+          stage[x * n + a] = x < cx ? elem(x0 + x, a) : 0.0;
+        }
+      } else {
+        for (int idx = threadIdx.x; idx < cx4 * n; idx += blockDim.x) {
+          const int a = idx % n, x = idx / n;
+          stage[x * n + a] = x < cx ? elem(x0 + x, a) : 0.0;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < kTpw; ++u) {
+        if (ti[u] < 0) continue;  // warp-uniform
+        const int ia = ti[u] + g, ja = tj[u] + g;
+        const bool iok = ia < n, jok = ja < n;
+        for (int x = 0; x < cx4; x += 4) {
+          const double* row = stage + (x + q) * n;
+          dmma_884(acc[u][0], acc[u][1], iok ? row[ia] : 0.0, jok ? row[ja] : 0.0);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kTpw; ++u) {
+      if (ti[u] < 0) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = ti[u] + g, j = tj[u] + 2 * q + h;
+        if (i < n && j < n) {
+          G[i + int64_t(j) * n] = acc[u][h];
+          G[j + int64_t(i) * n] = acc[u][h];
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
 template <class Elem>
 __device__ __forceinline__ void gram_tiled(int n, int64_t nx, Elem elem, bool x_fast, double* __restrict__ G,
                                            double* stage, int stage_cap) {
+#ifndef TT_NO_DMMA
+  if (n >= 16) {
+    gram_tiled_mma(n, nx, elem, x_fast, G, stage, stage_cap);
+    return;
+  }
+#endif
   const int nb = (n + 3) / 4;
   const int ntiles = nb * (nb + 1) / 2;
   const int ch = int(imax(1, imin(nx, stage_cap / n)));

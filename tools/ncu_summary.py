@@ -90,7 +90,11 @@ def main():
                 lines.append(f"| {label} (`{key}`) | {v} {u} |")
         rb, wb = to_bytes(m["dram__bytes_read.sum"]), to_bytes(m["dram__bytes_write.sum"])
         kern = name.split(":")[0]
-        traffic[kern] = rb + wb
+        if "/" in kern:  # "<workload>/<kind>": bench.py's per-workload traffic (e.g. c3_stream/leaf)
+            wl, kind = kern.split("/", 1)
+            traffic.setdefault(wl, {})[kind] = rb + wb
+        else:
+            traffic[kern] = rb + wb
         lines += ["", "Hottest source lines (warp-stall samples):", "", "```", top_lines(rep), "```"]
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     open(os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.md"), "w").write("\n".join(lines) + "\n")
