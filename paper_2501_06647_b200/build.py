@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libtucktree_b200.so")
-SOURCES = ["tt_leaf.cu", "tt_wide.cu", "tt_stitch.cu", "tt_stitch_wide.cu", "tt_host.cpp"]
+SOURCES = ["tt_leaf.cu", "tt_wide.cu", "tt_grid.cu", "tt_grid_solve.cu", "tt_stitch.cu", "tt_stitch_wide.cu", "tt_host.cpp"]
 HEADERS = ["tt_common.h", "tt_block.cuh", "tt_dev.cuh", "tt_stitch_body.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -38,10 +38,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
     common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", *extra,
               "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(ROOT, "include")]
     # one translation unit per kernel family, compiled in parallel, then linked
+    # (objects are kept, so a change to one source recompiles only that unit;
+    # a header change recompiles everything)
     objs, procs = [], []
+    hdr_t = max(os.path.getmtime(p) for p in [os.path.join(CSRC, h) for h in HEADERS]
+                + [os.path.join(ROOT, "include", "tucktree_b200.h"), os.path.abspath(__file__)])
+    tag = os.path.join(OUT_DIR, ".flags")
+    flags = " ".join(common)
+    if not os.path.exists(tag) or open(tag).read() != flags:
+        force = True
     for src in SOURCES:
         obj = os.path.join(OUT_DIR, os.path.splitext(src)[0] + ".o")
         objs.append(obj)
+        if (not force and os.path.exists(obj)
+                and os.path.getmtime(obj) > max(hdr_t, os.path.getmtime(os.path.join(CSRC, src)))):
+            continue
         procs.append(subprocess.Popen(common + ["-c", os.path.join(CSRC, src), "-o", obj],
                                       stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
     errs = []
@@ -59,6 +70,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed linking libtucktree_b200.so")
     os.replace(LIB + ".tmp", LIB)
+    with open(tag, "w") as f:
+        f.write(flags)
     return LIB
 
 

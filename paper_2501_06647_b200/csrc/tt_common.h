@@ -169,6 +169,67 @@ TT_HD LeafWs leaf_ws_layout(int p, int64_t len, const int64_t* d, const int64_t*
   return w;
 }
 
+// ---------------------------------------------------------------------------
+// Grid-wide leaf path (tt_grid.cu): wide batches of equal-length leaf blocks,
+// run as phase kernels over ALL leaves (streamed products split across the
+// whole GPU, per-leaf solver kernels in between).
+//
+// Tile of a streamed product out[o][a][t] = sum_j Ut[j][a] in[o][j][t]: each of
+// the 256 consumer threads owns tt consecutive columns t of one slab o and all
+// R accumulators; a tile is G slabs x tw columns, streamed in chunks of cj rows.
+struct GridTile {
+  int64_t tt, tw, tpo, G, cj, ngrp, ntt, njt;
+};
+constexpr int64_t kGridTileDoubles = 4096;  // X doubles per ring stage (32 KB)
+constexpr int64_t kGridCjMax = 16;          // rows of j per stage (bounds the staged U^T rows)
+constexpr int64_t kGridRcMax = 10;          // accumulator columns per thread (x tt columns of t)
+TT_HD GridTile grid_tile(int64_t outer, int64_t d, int64_t inner) {  // requires inner % 2 == 0
+  GridTile t;
+  t.tt = (inner % 4 == 0) ? 4 : 2;
+  t.tw = imin(inner, 256 * t.tt);
+  t.tpo = t.tw / t.tt;
+  t.G = imax(1, imin(outer, 256 / t.tpo));
+  t.cj = imax(1, imin(imin(d, kGridTileDoubles / (t.G * t.tw)), kGridCjMax));
+  t.ngrp = (outer + t.G - 1) / t.G;
+  t.ntt = (inner + t.tw - 1) / t.tw;
+  t.njt = (d + t.cj - 1) / t.cj;
+  return t;
+}
+// R accumulator columns are split into nchunk equal chunks of rc columns (even
+// when nchunk > 1, so every chunk starts 16-byte aligned); the staged U^T rows
+// are zero-padded to rp = nchunk*rc (rounded up to even) columns.
+struct GridChunks {
+  int nchunk, rc, rp;
+};
+TT_HD GridChunks grid_chunks(int64_t R) {
+  GridChunks c;
+  c.nchunk = int((R + kGridRcMax - 1) / kGridRcMax);
+  c.rc = int((R + c.nchunk - 1) / c.nchunk);
+  if (c.nchunk > 1) c.rc = (c.rc + 1) & ~1;
+  c.rp = (c.nchunk * c.rc + 1) & ~1;
+  return c;
+}
+// Extra per-leaf workspace behind leaf_ws_layout(): the row-major, zero-padded
+// U_1^T / U_0^T copies the streamed passes read (row stride grid_chunks(R).rp,
+// capacity 32 columns), per-tile partial
+// sums of ||X||^2, and the leaf's ALS state carried between the phase kernels.
+constexpr int64_t kGridUtLd = 32;
+enum { kGsNorm = 0, kGsPrevFit = 1, kGsDone = 2, kGsSweeps = 3, kGsConv = 4, kGsZero = 5, kGsK = 8, kGsSize = 16 };
+struct GridWs {
+  int64_t ut1, ut0, npart, state, total;
+};
+TT_HD GridWs grid_ws_layout(int p, int64_t len, const int64_t* d, const int64_t* req) {
+  const LeafWs l = leaf_ws_layout(p, len, d, req);
+  const GridTile t = grid_tile(len, d[1], prod_range(d, 2, p));
+  GridWs g;
+  g.ut1 = l.total;
+  g.ut0 = g.ut1 + d[1] * kGridUtLd;
+  g.npart = g.ut0 + len * kGridUtLd;
+  g.state = g.npart + ((t.ngrp * t.ntt + 1) & ~int64_t(1));
+  g.total = (g.state + kGsSize + 31) & ~int64_t(31);
+  return g;
+}
+
 struct StitchWs {
   int64_t P, C, S, E, A, G, V, T1, T2, TB1, TB2, Z, WK, HH, SI, misc, xch, gpart, total, gram_n;
   int64_t chain;  // per-part stride of the part-batched mode-product chains (TB1/TB2)

@@ -38,6 +38,10 @@ int stitch_wide_cluster();
 cudaError_t launch_stitch_wide(const Params& prm, const StitchDesc* d_descs, const StitchPart* d_parts, int n, int cs,
                                cudaStream_t st);
 cudaError_t launch_leaf_wide(const Params& prm, const LeafDesc* d_descs, int n, int cs, cudaStream_t st);
+// tt_grid.cu: grid-wide phase kernels for wide batches of equal-length leaves
+bool leaf_grid_ok(const Params& prm, int64_t len);
+cudaError_t launch_leaf_grid(const Params& prm, const LeafDesc* d_descs, int n, int64_t len, int* d_active,
+                             cudaStream_t st);
 cudaError_t launch_copy_segments(const CopySeg* d_segs, int n, cudaStream_t st);
 cudaError_t launch_partial_hit(const double* V0, int64_t ld, int64_t b, int64_t len, int n, const double* core,
                                int64_t rest, double* W, double* Q, double* R, double* out_core, double* tau,
@@ -355,13 +359,25 @@ std::vector<ProblemStatus> run_leaf_batch(Exec& ex, const Params& prm, std::vect
     wide = n <= 2 * std::max(1, nsm / cs);
     if (const char* e = std::getenv("TT_WIDE")) wide = e[0] == '1';
   }
+  // Batches of equal-length, 16-byte-aligned blocks: the grid-wide phase
+  // kernels (tt_grid.cu) stream X across the whole GPU. TT_GRID=0 disables the
+  // path, 1 keeps the cluster kernel for small batches, 2 (default) takes it
+  // for every eligible batch (A/B measurement).
+  int grid_mode = 2;
+  if (const char* e = std::getenv("TT_GRID")) grid_mode = std::atoi(e);
+  bool grid = grid_mode > 0 && (grid_mode >= 2 || !wide) && leaf_grid_ok(prm, descs[0].len);
+  for (int i = 0; grid && i < n; ++i)
+    grid = descs[i].len == descs[0].len && (reinterpret_cast<uintptr_t>(descs[i].x) & 15u) == 0;
+  if (grid) wide = false;
   std::vector<Index> wsz(ws_sizes);
   if (wide)  // + the per-CTA partial Gram slots of the cluster kernel
     for (int i = 0; i < n; ++i) wsz[i] = leaf_ws_layout(prm.p, descs[i].len, prm.d, prm.req, cs).total;
+  if (grid)  // + transposed factors, norm partials and the carried ALS state
+    for (int i = 0; i < n; ++i) wsz[i] = grid_ws_layout(prm.p, descs[i].len, prm.d, prm.req).total;
   size_t ws_total = 0;
   for (Index w : wsz) ws_total += static_cast<size_t>(w);
   ex.d_ws.ensure(ws_total * sizeof(double));
-  ex.d_status.ensure(size_t(n) * kStatusInts * sizeof(int32_t));
+  ex.d_status.ensure((size_t(n) * kStatusInts + size_t(prm.max_iters)) * sizeof(int32_t));
   ex.d_obj.ensure(size_t(n) * prm.max_iters * sizeof(double));
   size_t off = 0;
   for (int i = 0; i < n; ++i) {
@@ -371,7 +387,7 @@ std::vector<ProblemStatus> run_leaf_batch(Exec& ex, const Params& prm, std::vect
     descs[i].objective = ex.d_obj.as<double>() + size_t(i) * prm.max_iters;
   }
   // TMA tensor maps (two per leaf, 64-byte aligned) for the streamed X passes
-  if (prm.p >= 2) {
+  if (prm.p >= 2 && !grid) {
     std::vector<CUtensorMap> maps(size_t(2) * n);
     ex.d_tmaps.ensure(sizeof(CUtensorMap) * 2 * n + 128);
     CUtensorMap* dmaps = reinterpret_cast<CUtensorMap*>((reinterpret_cast<uintptr_t>(ex.d_tmaps.p) + 127) & ~uintptr_t(127));
@@ -387,7 +403,11 @@ std::vector<ProblemStatus> run_leaf_batch(Exec& ex, const Params& prm, std::vect
   ex.d_desc.ensure(sizeof(LeafDesc) * n);
   cuda_check(cudaMemcpyAsync(ex.d_desc.p, descs.data(), sizeof(LeafDesc) * n, cudaMemcpyHostToDevice, ex.stream),
              "upload leaf descriptors");
-  if (wide)
+  if (grid)
+    cuda_check(launch_leaf_grid(prm, ex.d_desc.as<LeafDesc>(), n, descs[0].len,
+                                ex.d_status.as<int32_t>() + size_t(n) * kStatusInts, ex.stream),
+               "grid leaf kernels");
+  else if (wide)
     cuda_check(launch_leaf_wide(prm, ex.d_desc.as<LeafDesc>(), n, cs, ex.stream), "leaf_wide_kernel launch");
   else
     cuda_check(launch_leaf(prm, ex.d_desc.as<LeafDesc>(), n, ex.stream), "leaf_als_kernel launch");
