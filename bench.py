@@ -302,6 +302,7 @@ def run_engine(args, rank, world, local_rank):
         "e2e": {"value": round(e2e_qps, 3), "unit": "queries/s", "h2d_bytes_per_step": int(x.nbytes),
                 "d2h_bytes_per_step": int(out_bytes), "append_slices_per_s": round(e2e_sps, 3)},
         "roofline": roof,
+        "stream_pass": pass_roof(step_pass, build_pass, peak),
         "gpu_launches": int(launches),
         "solver_per_step": solver,
         "clocks": clk.summary(),
@@ -533,10 +534,13 @@ def run_engine_stream(args, rank, world, local_rank):
     warm.append_device(xd.data_ptr(), T0)
     del warm
     torch.cuda.synchronize()
+    sp0 = eng.stream_pass_stats()
     b0 = time.perf_counter()
     tree.append_device(xd.data_ptr(), T0)
     build_s = time.perf_counter() - b0
     build_ms = tree.last_timing_ms()
+    sp1 = eng.stream_pass_stats()
+    build_pass = {k: sp1[k] - sp0[k] for k in sp0}
     tree_e.append_device(xd.data_ptr(), T0)
     torch.cuda.synchronize()
     acc = {"leaf": 0.0, "stitch": 0.0, "tail": 0.0, "qstitch": 0.0}
@@ -599,6 +603,7 @@ def run_engine_stream(args, rank, world, local_rank):
     torch.cuda.synchronize()
     launches0 = eng.kernel_launches()
     stats0 = eng.solver_stats()
+    sp0 = eng.stream_pass_stats()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
@@ -609,6 +614,8 @@ def run_engine_stream(args, rank, world, local_rank):
         torch.cuda.synchronize()
     span_ms = ev0.elapsed_time(ev1)
     launches = eng.kernel_launches() - launches0
+    sp1 = eng.stream_pass_stats()
+    step_pass = {k: sp1[k] - sp0[k] for k in sp0}
     stats1 = eng.solver_stats()
     solver = {k: (stats1[k] - stats0[k]) / K for k in ("problems", "als_sweeps", "eig_calls", "jacobi_sweeps",
                                                        "subspace_ok", "subspace_fallback", "subspace_iters")}
@@ -651,7 +658,8 @@ def run_engine_stream(args, rank, world, local_rank):
                 "peak_kind": peak_kind}
     else:
         gbs = alg["leaf"] / (t_leafk / 1e3) / 1e9
-        roof = {"kernel": "leaf_wide_kernel (streamed leaf blocks + query tails)", "bound": "hbm",
+        roof = {"kernel": "grid-wide leaf ALS (grid_ttm/grid_last/grid_gram + grid_solve kernels: streamed leaf "
+                          "blocks + query tails)", "bound": "hbm",
                 "achieved": round(gbs, 3), "peak": peak, "unit": "GB/s", "frac": round(gbs / peak, 6),
                 "traffic": traffic.get("leaf"), "algorithmic_bytes_per_step": alg["leaf"] // K,
                 "peak_kind": peak_kind}
@@ -696,6 +704,7 @@ def run_engine_stream(args, rank, world, local_rank):
                 "h2d_bytes_per_step": int(B * ss * 8), "d2h_bytes_per_step": int(q_out_bytes // K),
                 "append_slices_per_s": round(world * K * B / (e2e_ms / 1e3), 3)},
         "roofline": roof,
+        "stream_pass": pass_roof(step_pass, build_pass, peak),
         "gpu_launches": int(launches),
         "solver_per_step": solver,
         "clocks": clk.summary(),
@@ -705,6 +714,22 @@ def run_engine_stream(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def pass_roof(step_pass, build_pass, peak):
+    """Achieved HBM bandwidth of grid_ttm_kernel's passes over X (the only kernel
+    of the path that moves leaf-block-sized data), from the engine's CUDA events
+    around each launch: inside the timed steps (one leaf block or query tail per
+    launch, L2-resident after the first pass) and in the 192-leaf build
+    (4.3 GB per launch, from HBM)."""
+    out = {"kernel": "grid_ttm_kernel (X x_1 U_1^T and X x_0 U_0^T passes)", "bound": "hbm", "unit": "GB/s", "peak": peak}
+    for tag, sp in (("steps", step_pass), ("build", build_pass)):
+        if sp["launches"] > 0 and sp["ms"] > 0:
+            gbs = sp["bytes"] / (sp["ms"] / 1e3) / 1e9
+            out[tag] = {"launches": int(sp["launches"]), "avg_launch_ms": round(sp["ms"] / sp["launches"], 4),
+                        "bytes_per_launch": int(sp["bytes"] / sp["launches"]), "achieved": round(gbs, 1),
+                        "frac": round(gbs / peak, 4)}
+    return out
 
 
 def load_traffic(key):

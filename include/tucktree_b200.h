@@ -278,6 +278,12 @@ int64_t tt_kernel_launches(void);
  * A Y + residual, CholeskyQR2, Rayleigh-Ritz). Entries [0..18] count leaf
  * (tucker_als) problems, [19..37] stitch problems.                        */
 void tt_solver_stats(int64_t* out38);
+/* Cumulative device time of the grid-wide leaf path's streamed passes over X
+ * (grid_ttm_kernel passes 1 and 2; CUDA events on the launching stream):
+ * [0] launches, [1] milliseconds, [2] bytes of X read (8 * leaves * B * prod D
+ * per launch: the algorithmic bytes of the pass). The bench reports the delta
+ * over its timed region as the kernel's achieved HBM bandwidth.            */
+void tt_stream_pass_stats(double* out3);
 
 #ifdef __cplusplus
 }

@@ -3,6 +3,6 @@
 mirror of the reference API in tucktree.py."""
 from .tucktree import (  # noqa: F401
     ENTIRE, INTERMEDIATE, LEAF, PARTIAL, PLACEHOLDER, TAIL, CudaError, HitEntry, InvalidArgument, LogicError, Node,
-    QueryResult, StreamSegmentTree, brute_force_batch, partial_hit_factors, brute_force_range, relative_error, TuckerFactors, kernel_launches, lib, lib_path, read_tensor, solver_stats, stitch,
+    QueryResult, StreamSegmentTree, brute_force_batch, partial_hit_factors, brute_force_range, relative_error, TuckerFactors, kernel_launches, lib, lib_path, read_tensor, solver_stats, stitch, stream_pass_stats,
     tucker_als, write_tensor,
 )

@@ -20,19 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
-        return True
-    t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
-    deps.append(os.path.join(ROOT, "include", "tucktree_b200.h"))
-    deps.append(os.path.abspath(__file__))
-    return any(os.path.getmtime(p) > t for p in deps)
-
-
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
     extra = ["-DTT_INSTRUMENT"] if os.environ.get("TT_INSTRUMENT") == "1" else []
     common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", *extra,
@@ -41,8 +29,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     # (objects are kept, so a change to one source recompiles only that unit;
     # a header change recompiles everything)
     objs, procs = [], []
-    hdr_t = max(os.path.getmtime(p) for p in [os.path.join(CSRC, h) for h in HEADERS]
-                + [os.path.join(ROOT, "include", "tucktree_b200.h"), os.path.abspath(__file__)])
+    hdr_t = max(os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS)  # (flag changes: the .flags tag)
+    api_t = os.path.getmtime(os.path.join(ROOT, "include", "tucktree_b200.h"))  # included by tt_host.cpp only
     tag = os.path.join(OUT_DIR, ".flags")
     flags = " ".join(common)
     if not os.path.exists(tag) or open(tag).read() != flags:
@@ -51,10 +39,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(OUT_DIR, os.path.splitext(src)[0] + ".o")
         objs.append(obj)
         if (not force and os.path.exists(obj)
-                and os.path.getmtime(obj) > max(hdr_t, os.path.getmtime(os.path.join(CSRC, src)))):
+                and os.path.getmtime(obj) > max(hdr_t, os.path.getmtime(os.path.join(CSRC, src)),
+                                                api_t if src == "tt_host.cpp" else 0)):
             continue
         procs.append(subprocess.Popen(common + ["-c", os.path.join(CSRC, src), "-o", obj],
                                       stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
+    if not procs and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(o) for o in objs):
+        return LIB  # nothing changed
     errs = []
     for pr in procs:
         out, err = pr.communicate()

@@ -183,12 +183,14 @@ struct GridTile {
 constexpr int64_t kGridTileDoubles = 4096;  // X doubles per ring stage (32 KB)
 constexpr int64_t kGridCjMax = 16;          // rows of j per stage (bounds the staged U^T rows)
 constexpr int64_t kGridRcMax = 10;          // accumulator columns per thread (x tt columns of t)
-TT_HD GridTile grid_tile(int64_t outer, int64_t d, int64_t inner) {  // requires inner % 2 == 0
+// gcap bounds the slabs per tile: small batches take fewer slabs per tile so the
+// pass has enough work items for every SM.
+TT_HD GridTile grid_tile(int64_t outer, int64_t d, int64_t inner, int64_t gcap = 256) {  // requires inner % 2 == 0
   GridTile t;
   t.tt = (inner % 4 == 0) ? 4 : 2;
   t.tw = imin(inner, 256 * t.tt);
   t.tpo = t.tw / t.tt;
-  t.G = imax(1, imin(outer, 256 / t.tpo));
+  t.G = imax(1, imin(imin(outer, 256 / t.tpo), gcap));
   t.cj = imax(1, imin(imin(d, kGridTileDoubles / (t.G * t.tw)), kGridCjMax));
   t.ngrp = (outer + t.G - 1) / t.G;
   t.ntt = (inner + t.tw - 1) / t.tw;
@@ -215,18 +217,20 @@ TT_HD GridChunks grid_chunks(int64_t R) {
 // sums of ||X||^2, and the leaf's ALS state carried between the phase kernels.
 constexpr int64_t kGridUtLd = 32;
 enum { kGsNorm = 0, kGsPrevFit = 1, kGsDone = 2, kGsSweeps = 3, kGsConv = 4, kGsZero = 5, kGsK = 8, kGsSize = 16 };
+constexpr int64_t kGridGramCtas = 16;  // row chunks (CTAs) of a grid-wide partial Gram per leaf
 struct GridWs {
-  int64_t ut1, ut0, npart, state, total;
+  int64_t ut1, ut0, npart, state, gpart, total;
 };
 TT_HD GridWs grid_ws_layout(int p, int64_t len, const int64_t* d, const int64_t* req) {
   const LeafWs l = leaf_ws_layout(p, len, d, req);
-  const GridTile t = grid_tile(len, d[1], prod_range(d, 2, p));
+  const GridTile t = grid_tile(len, d[1], prod_range(d, 2, p), 1);  // most tiles: one slab each
   GridWs g;
   g.ut1 = l.total;
   g.ut0 = g.ut1 + d[1] * kGridUtLd;
   g.npart = g.ut0 + len * kGridUtLd;
   g.state = g.npart + ((t.ngrp * t.ntt + 1) & ~int64_t(1));
-  g.total = (g.state + kGsSize + 31) & ~int64_t(31);
+  g.gpart = (g.state + kGsSize + 31) & ~int64_t(31);  // kGridGramCtas partial Grams (gram_n^2 each)
+  g.total = (g.gpart + kGridGramCtas * l.gram_n * l.gram_n + 31) & ~int64_t(31);
   return g;
 }
 

@@ -69,7 +69,7 @@ __host__ __device__ __forceinline__ GridPassShape grid_pass_shape(const Params& 
 template <int RC, int TT>
 __global__ void __launch_bounds__(kGridThreads, 1)
 grid_ttm_kernel(Params prm, const LeafDesc* __restrict__ descs, int nleaves, int pass, int R, int want_norm,
-                int k0) {
+                int k0, int gcap) {
   __shared__ GridPipe pipe;
   __shared__ double red[8];
   extern __shared__ __align__(128) double dsm[];
@@ -83,7 +83,7 @@ grid_ttm_kernel(Params prm, const LeafDesc* __restrict__ descs, int nleaves, int
   __syncthreads();
   const int64_t len = descs[0].len;  // equal-length batch
   const GridPassShape sh = grid_pass_shape(prm, len, pass, k0);
-  const GridTile tile = grid_tile(sh.outer, sh.d, sh.inner);
+  const GridTile tile = grid_tile(sh.outer, sh.d, sh.inner, gcap);
   const GridChunks ch = grid_chunks(R);
   const LeafWs lay = leaf_ws_layout(prm.p, len, prm.d, prm.req);
   const GridWs gw = grid_ws_layout(prm.p, len, prm.d, prm.req);
@@ -218,9 +218,11 @@ grid_ttm_kernel(Params prm, const LeafDesc* __restrict__ descs, int nleaves, int
   }
 }
 
-// Last-mode contraction of W for order-3 series: out[c][a] = sum_t W[c][t] U[t][a]
-// over the k0*D_1 rows c of every leaf (the first product of mode 1,
-// W x_2 U_2^T). A CTA stages 128 contiguous rows (padded against bank
+// Last-mode contraction of W for order-3 series: sum_t W[c][t] U[t][a] over the
+// k0*D_1 rows c = (o, j) of every leaf (the first product of mode 1,
+// W x_2 U_2^T), written as the mode-1 unfolding itself: a dense row-major
+// D_1 x (k0*R) matrix out[j][o*R + a], so the solver's Gram, warm start and
+// back-multiplication read contiguous rows. A CTA stages 128 contiguous rows (padded against bank
 // conflicts) and U^T in shared memory; a thread owns one row and half of the
 // R columns.
 constexpr int kLastRows = 128;
@@ -266,7 +268,8 @@ grid_last_kernel(Params prm, const LeafDesc* __restrict__ descs, int64_t rows, i
 #pragma unroll
     for (int a = 0; a < RH; ++a) acc[a] = fma(ur[t * rp + a], x, acc[a]);
   }
-  double* out = D.ws + lay.B1 + (c0 + r) * R + a0;
+  const int64_t c = c0 + r, d1 = prm.d[1], o = c / d1, j = c - o * d1;
+  double* out = D.ws + lay.B1 + j * (rows / d1) * R + o * R + a0;
 #pragma unroll
   for (int a = 0; a < RH; ++a)
     if (a0 + a < R) out[a] = acc[a];
@@ -274,12 +277,14 @@ grid_last_kernel(Params prm, const LeafDesc* __restrict__ descs, int64_t rows, i
 
 cudaError_t grid_solve_prepare();
 void launch_grid_prep(const Params& prm, const LeafDesc* d_descs, int n, int* d_active, cudaStream_t st);
-void launch_grid_solve0(const Params& prm, const LeafDesc* d_descs, int n, int sweep, cudaStream_t st);
+void launch_grid_solve0(const Params& prm, const LeafDesc* d_descs, int n, int sweep, int gcap, cudaStream_t st);
 void launch_grid_solve_mode(const Params& prm, const LeafDesc* d_descs, int n, int sweep, int mode, int first_done,
-                            int* d_active, cudaStream_t st);
+                            int gram_ready, int* d_active, cudaStream_t st);
+bool grid_gram_applies(int64_t rows, int64_t cols, int64_t k);
+void launch_grid_gram(const Params& prm, const LeafDesc* d_descs, int n, int cols, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
-using GridTtmFn = void (*)(Params, const LeafDesc*, int, int, int, int, int);
+using GridTtmFn = void (*)(Params, const LeafDesc*, int, int, int, int, int, int);
 template <int TT>
 static GridTtmFn grid_ttm_fn(int rc) {
   switch (rc) {
@@ -307,6 +312,30 @@ static GridLastFn grid_last_fn(int rh) {
   }
 }
 constexpr size_t kLastDynSmem = size_t(kLastRows * (kLastMaxD + 2) + kLastMaxD * 32) * sizeof(double);  // 120 KB cap
+
+// Device time of the streamed passes over X (passes 1 and 2), for the bench's
+// live roofline: events around each launch, read after the sweep's sync.
+static std::mutex g_pass_mu;
+static double g_pass_stats[3] = {0.0, 0.0, 0.0};  // launches, ms, X bytes
+void grid_pass_stats(double* out3) {
+  std::lock_guard<std::mutex> lk(g_pass_mu);
+  for (int i = 0; i < 3; ++i) out3[i] = g_pass_stats[i];
+}
+struct PassEvents {
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  int dev = -1;
+  bool ensure() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) return false;
+    if (d == dev) return true;
+    for (auto& e : ev) {
+      if (e) cudaEventDestroy(e);
+      if (cudaEventCreate(&e) != cudaSuccess) return false;
+    }
+    dev = d;
+    return true;
+  }
+};
 
 // Per-device launch state: shared-memory caps set once, resident CTA count.
 static cudaError_t grid_prepare(int* ctas_out) {
@@ -367,15 +396,21 @@ cudaError_t launch_leaf_grid(const Params& prm, const LeafDesc* d_descs, int n, 
   for (int m = 1; m < p; ++m) d[m] = prm.d[m];
   clamp_ranks(p, d, prm.req, k);
   launch_grid_prep(prm, d_descs, n, d_active, st);
+  static thread_local PassEvents pe;
+  const bool timed = pe.ensure();
   auto ttm = [&](int pass, int64_t R, int want_norm) -> cudaError_t {
     const GridPassShape sh = grid_pass_shape(prm, len, pass, k[0]);
-    const GridTile t = grid_tile(sh.outer, sh.d, sh.inner);
+    // slabs per tile: enough items for two per SM when the batch is small
+    const int64_t gcap = imax(1, sh.outer * n / (2 * ctas));
+    const GridTile t = grid_tile(sh.outer, sh.d, sh.inner, gcap);
     const GridChunks ch = grid_chunks(R);
     const int64_t items = int64_t(ch.nchunk) * t.ngrp * t.ntt * n;
     GridTtmFn fn = t.tt == 4 ? grid_ttm_fn<4>(ch.rc) : grid_ttm_fn<2>(ch.rc);
     if (!fn) return cudaErrorInvalidValue;
+    if (timed && pass <= 2) cudaEventRecord(pe.ev[2 * (pass - 1)], st);
     fn<<<unsigned(imin(items, ctas)), kGridThreads, kGridDynSmem, st>>>(prm, d_descs, n, pass, int(R), want_norm,
-                                                                         int(k[0]));
+                                                                         int(k[0]), int(gcap));
+    if (timed && pass <= 2) cudaEventRecord(pe.ev[2 * (pass - 1) + 1], st);
     g_launches.fetch_add(1);
     return cudaGetLastError();
   };
@@ -391,27 +426,45 @@ cudaError_t launch_leaf_grid(const Params& prm, const LeafDesc* d_descs, int n, 
     g_launches.fetch_add(1);
     return cudaGetLastError();
   };
+  int prev_left = n;
   for (int sweep = 0; sweep < prm.max_iters; ++sweep) {
     if ((e = ttm(1, k[1], sweep == 0)) != cudaSuccess) return e;
-    launch_grid_solve0(prm, d_descs, n, sweep, st);
+    launch_grid_solve0(prm, d_descs, n, sweep, int(imax(1, len * n / (2 * ctas))), st);
     k[0] = leaf_mode_rank(p, d, k, 0);
     if ((e = ttm(2, k[0], 0)) != cudaSuccess) return e;
     for (int m = 1; m < p; ++m) {
       // the W-sized first product of the mode's chain, grid-wide where a kernel covers its shape
-      int first_done = 0;
+      int first_done = 0, gram_ready = 0;
       if (m >= 2) {
         if ((e = ttm(3, k[1], 0)) != cudaSuccess) return e;
         first_done = 1;
       } else if (p == 3 && d[2] <= kLastMaxD && d[2] % 2 == 0 && k[2] <= 32) {
         if ((e = last()) != cudaSuccess) return e;
         first_done = 1;
+        // its Gram, split over row chunks across the GPU
+        if (grid_gram_applies(d[1], k[0] * k[2], leaf_mode_rank(p, d, k, 1))) {
+          launch_grid_gram(prm, d_descs, n, int(k[0] * k[2]), st);
+          gram_ready = 1;
+        }
       }
-      launch_grid_solve_mode(prm, d_descs, n, sweep, m, first_done, d_active, st);
+      launch_grid_solve_mode(prm, d_descs, n, sweep, m, first_done, gram_ready, d_active, st);
       k[m] = leaf_mode_rank(p, d, k, m);
     }
     int left = 0;
     if ((e = cudaMemcpyAsync(&left, d_active + sweep, sizeof(int), cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+    if (timed) {  // converged leaves are skipped: count the leaves this sweep streamed
+      const int streamed = sweep == 0 ? n : prev_left;
+      float ms1 = 0.f, ms2 = 0.f;
+      if (cudaEventElapsedTime(&ms1, pe.ev[0], pe.ev[1]) == cudaSuccess &&
+          cudaEventElapsedTime(&ms2, pe.ev[2], pe.ev[3]) == cudaSuccess) {
+        std::lock_guard<std::mutex> lk(g_pass_mu);
+        g_pass_stats[0] += 2.0;
+        g_pass_stats[1] += double(ms1) + double(ms2);
+        g_pass_stats[2] += 2.0 * 8.0 * double(streamed) * double(len) * double(prod_range(d, 1, p));
+      }
+    }
+    prev_left = left;
     if (left == 0) break;
   }
   return cudaGetLastError();

@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kThreads) grid_prep_kernel(Params prm, const L
 
 // After pass 1: the remaining contractions of Y, then U_0 = llsv(M_0(Y)).
 __global__ void __launch_bounds__(kThreads, 2) grid_solve0_kernel(Params prm, const LeafDesc* __restrict__ descs,
-                                                                  int sweep) {
+                                                                  int sweep, int gcap) {
   __shared__ BlockScratch sc;
   extern __shared__ __align__(128) double dsm[];
   const LeafDesc D = descs[blockIdx.x];
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kThreads, 2) grid_solve0_kernel(Params prm, co
   for (int m = 0; m < p; ++m) k[m] = int64_t(st[kGsK + m]);
   double* B[2] = {D.ws + lay.B1, D.ws + lay.B2};
   if (sweep == 0) {
-    const GridTile t1 = grid_tile(D.len, prm.d[1], prod_range(prm.d, 2, p));
+    const GridTile t1 = grid_tile(D.len, prm.d[1], prod_range(prm.d, 2, p), gcap);
     double s = 0.0;
     if (threadIdx.x == 0)
       for (int64_t i = 0; i < t1.ngrp * t1.ntt; ++i) s += D.ws[gw.npart + i];
@@ -125,13 +125,38 @@ __global__ void __launch_bounds__(kThreads, 2) grid_solve0_kernel(Params prm, co
   grid_status(D, st, p, sc);
 }
 
+// Partial Grams A^T A of the dense mode-1 unfolding (D_1 x cols, row-major in B1,
+// written by grid_last_kernel) over kGridGramCtas row chunks per leaf:
+// blockIdx.x = chunk, blockIdx.y = leaf. grid_solve_mode_kernel sums the
+// partials in chunk order (bit-identical across runs) and goes straight to the
+// eigensolver (the cluster kernel's wide_llsv, spread over the grid).
+__global__ void __launch_bounds__(kThreads, 2) grid_gram_kernel(Params prm, const LeafDesc* __restrict__ descs,
+                                                                int cols) {
+  extern __shared__ __align__(128) double dsm[];
+  const LeafDesc D = descs[blockIdx.y];
+  const int p = prm.p;
+  const LeafWs lay = leaf_ws_layout(p, D.len, prm.d, prm.req);
+  const GridWs gw = grid_ws_layout(p, D.len, prm.d, prm.req);
+  if (D.ws[gw.state + kGsDone] != 0.0) return;
+  const int64_t rows = prm.d[1], per = (rows + gridDim.x - 1) / gridDim.x;
+  const int64_t x0 = imin(rows, int64_t(blockIdx.x) * per), x1 = imin(rows, x0 + per);
+  const double* A = D.ws + lay.B1;
+  double* Gp = D.ws + gw.gpart + int64_t(blockIdx.x) * cols * cols;
+  if (x1 <= x0) {
+    for (int64_t idx = threadIdx.x; idx < int64_t(cols) * cols; idx += blockDim.x) Gp[idx] = 0.0;
+    return;
+  }
+  gram_tiled(cols, x1 - x0, [&](int64_t i, int a) { return A[(x0 + i) * cols + a]; }, false, Gp, dsm,
+             int(dyn_smem_doubles()));
+}
+
 // After pass 2, once per mode n >= 1: the contraction chain W x_{m != 0,n} U_m^T
 // (its first, W-sized product already in B1 when `first_done`: computed
 // grid-wide by tt_grid.cu), then U_n = llsv. The last mode's call also forms
 // the core, the fit and the stop test (tucker.cpp:67-76, 104-116).
 __global__ void __launch_bounds__(kThreads, 2) grid_solve_mode_kernel(Params prm, const LeafDesc* __restrict__ descs,
                                                                       int sweep, int n, int first_done,
-                                                                      int* __restrict__ active) {
+                                                                      int gram_ready, int* __restrict__ active) {
   __shared__ BlockScratch sc;
   extern __shared__ __align__(128) double dsm[];
   const LeafDesc D = descs[blockIdx.x];
@@ -164,8 +189,23 @@ __global__ void __launch_bounds__(kThreads, 2) grid_solve_mode_kernel(Params prm
     s2 = dst;
     t2 ^= 1;
   }
-  llsv_unfold(s2, prod_range(pc, 0, n), d[n], prod_range(pc, n + 1, p), kn, D.out_f[n], D.ws + lay.G, D.ws + lay.V,
-              D.ws + lay.misc, dsm, sc, k[n], D.ws + lay.SI);
+  if (first_done && n == 1 && p == 3) {  // grid_last_kernel wrote the unfolding as a dense D_1 x (k0*k2) matrix
+    const int64_t cols = pc[0] * pc[2];
+    if (gram_ready) {  // grid_gram_kernel's partials, summed in chunk order
+      double* G = D.ws + lay.G;
+      const double* gp = D.ws + gw.gpart;
+      for (int64_t idx = threadIdx.x; idx < cols * cols; idx += blockDim.x) {
+        double v = 0.0;
+        for (int r = 0; r < int(kGridGramCtas); ++r) v += gp[int64_t(r) * cols * cols + idx];
+        G[idx] = v;
+      }
+      __syncthreads();
+    }
+    llsv_unfold(s2, 1, d[1], cols, kn, D.out_f[1], D.ws + lay.G, D.ws + lay.V, D.ws + lay.misc, dsm, sc, k[1],
+                D.ws + lay.SI, gram_ready != 0);
+  } else
+    llsv_unfold(s2, prod_range(pc, 0, n), d[n], prod_range(pc, n + 1, p), kn, D.out_f[n], D.ws + lay.G, D.ws + lay.V,
+                D.ws + lay.misc, dsm, sc, k[n], D.ws + lay.SI);
   k[n] = kn;
   if (n == 1) write_ut(D.out_f[1], d[1], k[1], D.ws + gw.ut1);
   if (threadIdx.x == 0) st[kGsK + n] = double(kn);
@@ -218,6 +258,8 @@ cudaError_t grid_solve_prepare() {
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(grid_solve_mode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kGridSolveSmemBig));
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(grid_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kLeafDynSmem));
+  if (e != cudaSuccess) return e;
   done |= uint64_t(1) << (dev & 63);
   return cudaSuccess;
 }
@@ -225,13 +267,25 @@ void launch_grid_prep(const Params& prm, const LeafDesc* d_descs, int n, int* d_
   grid_prep_kernel<<<n, kThreads, 0, st>>>(prm, d_descs, d_active);
   g_launches.fetch_add(1);
 }
-void launch_grid_solve0(const Params& prm, const LeafDesc* d_descs, int n, int sweep, cudaStream_t st) {
-  grid_solve0_kernel<<<n, kThreads, grid_solve_smem(n), st>>>(prm, d_descs, sweep);
+void launch_grid_solve0(const Params& prm, const LeafDesc* d_descs, int n, int sweep, int gcap, cudaStream_t st) {
+  grid_solve0_kernel<<<n, kThreads, grid_solve_smem(n), st>>>(prm, d_descs, sweep, gcap);
   g_launches.fetch_add(1);
 }
 void launch_grid_solve_mode(const Params& prm, const LeafDesc* d_descs, int n, int sweep, int mode, int first_done,
-                            int* d_active, cudaStream_t st) {
-  grid_solve_mode_kernel<<<n, kThreads, grid_solve_smem(n), st>>>(prm, d_descs, sweep, mode, first_done, d_active);
+                            int gram_ready, int* d_active, cudaStream_t st) {
+  grid_solve_mode_kernel<<<n, kThreads, grid_solve_smem(n), st>>>(prm, d_descs, sweep, mode, first_done, gram_ready,
+                                                                 d_active);
+  g_launches.fetch_add(1);
+}
+// Whether the mode-1 Gram of a dense rows x cols unfolding (k columns wanted) is
+// formed grid-wide: exactly when llsv_unfold would take its tiled-Gram route
+// (tall, no tall subspace iteration: see llsv_uses_subspace).
+bool grid_gram_applies(int64_t rows, int64_t cols, int64_t k) {
+  const bool tall_si = cols >= 2 * k && cols * k <= kSiMaxYK && k <= kSiMaxK;
+  return rows > cols && !tall_si && cols >= kGramTiledMinN && cols * 4 <= int64_t(kLeafDynSmem / sizeof(double));
+}
+void launch_grid_gram(const Params& prm, const LeafDesc* d_descs, int n, int cols, cudaStream_t st) {
+  grid_gram_kernel<<<dim3(unsigned(kGridGramCtas), unsigned(n)), kThreads, kLeafDynSmem, st>>>(prm, d_descs, cols);
   g_launches.fetch_add(1);
 }
 

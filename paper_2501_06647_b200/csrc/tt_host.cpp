@@ -40,6 +40,7 @@ cudaError_t launch_stitch_wide(const Params& prm, const StitchDesc* d_descs, con
 cudaError_t launch_leaf_wide(const Params& prm, const LeafDesc* d_descs, int n, int cs, cudaStream_t st);
 // tt_grid.cu: grid-wide phase kernels for wide batches of equal-length leaves
 bool leaf_grid_ok(const Params& prm, int64_t len);
+void grid_pass_stats(double* out3);
 cudaError_t launch_leaf_grid(const Params& prm, const LeafDesc* d_descs, int n, int64_t len, int* d_active,
                              cudaStream_t st);
 cudaError_t launch_copy_segments(const CopySeg* d_segs, int n, cudaStream_t st);
@@ -968,6 +969,7 @@ const char* tt_last_error(void) { return g_err.c_str(); }
 const char* tt_version(void) { return "tucktree_b200 0.2 (sm_100a)"; }
 void tt_debug_fail_appends(int32_t n) { g_fail_appends.store(n); }
 int64_t tt_kernel_launches(void) { return launches(); }
+void tt_stream_pass_stats(double* out3) { ttb::grid_pass_stats(out3); }
 void tt_solver_stats(int64_t* out38) {
   for (int k = 0; k < 2; ++k)
     for (int i = 0; i < 19; ++i) out38[k * 19 + i] = g_stats[k][i];

@@ -64,6 +64,7 @@ SIGNATURES = {
     "tt_version": (C.c_char_p, []),
     "tt_kernel_launches": (i64, []),
     "tt_solver_stats": (None, [i64ptr]),
+    "tt_stream_pass_stats": (None, [dptr]),
     "tt_tree_create": (C.c_int, [C.POINTER(TTConfig), C.POINTER(vp)]),
     "tt_tree_destroy": (None, [vp]),
     "tt_tree_clear": (C.c_int, [vp]),
@@ -613,6 +614,13 @@ def read_tensor(path: str) -> np.ndarray:
 
 def kernel_launches() -> int:
     return lib().tt_kernel_launches()
+
+
+def stream_pass_stats() -> dict:
+    """Cumulative launches / device ms / X bytes of the grid-wide leaf path's streamed passes."""
+    out = np.zeros(3, dtype=np.float64)
+    lib().tt_stream_pass_stats(out.ctypes.data_as(dptr))
+    return {"launches": int(out[0]), "ms": float(out[1]), "bytes": float(out[2])}
 
 
 def solver_stats() -> dict:
