@@ -301,6 +301,7 @@ static __device__ void chol_inv_warp(const double* G, int k, double* L, double* 
   double dmax = 0.0;
   for (int j = 0; j < k; ++j) dmax = fmax(dmax, G[j + j * k]);
   bool ok = dmax > 0.0;
+  double myinv = 0.0;  // lane j keeps 1 / L(j, j)
   for (int j = 0; j < k && ok; ++j) {
     double sdiag = 0.0;
     if (lane == j) {
@@ -314,26 +315,36 @@ static __device__ void chol_inv_warp(const double* G, int k, double* L, double* 
       ok = false;
       break;
     }
-    const double ljj = sqrt(sdiag), inv = 1.0 / ljj;
+    // one rsqrt instead of sqrt + divide on the serial chain (64 vs 158 cycles)
+    const double inv = rsqrt(sdiag), ljj = sdiag * inv;
     if (lane > j && lane < k) {
       double v = G[lane + j * k];
       for (int l = 0; l < j; ++l) v -= L[lane + l * k] * L[j + l * k];
       L[lane + j * k] = v * inv;
     }
-    if (lane == j) L[j + j * k] = ljj;
+    if (lane == j) {
+      L[j + j * k] = ljj;
+      myinv = inv;
+    }
     __syncwarp();
   }
   if (!ok) {
     if (lane == 0) sc.ibcast[2] = 1;
     return;
   }
-  if (lane < k) {  // column `lane` of L^{-1} by forward substitution
-    const int c = lane;
-    for (int i = 0; i < c; ++i) Linv[i + c * k] = 0.0;
-    for (int i = c; i < k; ++i) {
-      double v = (i == c) ? 1.0 : 0.0;
-      for (int l = c; l < i; ++l) v -= L[i + l * k] * Linv[l + c * k];
-      Linv[i + c * k] = v / L[i + i * k];
+  // column `lane` of L^{-1} by forward substitution (reciprocal diagonals
+  // broadcast by shuffle: no divides on the chain)
+  for (int i = 0; i < k; ++i) {
+    const double invd = __shfl_sync(0xffffffffu, myinv, i);
+    if (lane < k) {
+      const int c = lane;
+      if (i < c) {
+        Linv[i + c * k] = 0.0;
+      } else {
+        double v = (i == c) ? 1.0 : 0.0;
+        for (int l = c; l < i; ++l) v -= L[i + l * k] * Linv[l + c * k];
+        Linv[i + c * k] = v * invd;
+      }
     }
   }
 }
@@ -733,6 +744,82 @@ __device__ __forceinline__ bool llsv_uses_subspace(int64_t rows, int64_t cols, i
   return si != nullptr && kprev > 0 && rows > cols && cols >= 2 * k && cols * k <= kSiMaxYK && k <= kSiMaxK &&
          si_base() + kSiMaxYK + 5 * k * k + 256 <= sc.dsm_cap;
 }
+// Y (n x kp, ld n) = A^T U for a dense row-major A (rows x n, n <= blockDim.x)
+// and U (rows x kp, ld rows): a thread owns one column of A in one of
+// blockDim.x / n row groups and 8 columns of U at a time (coalesced loads of
+// A, broadcast loads of U); the row groups' partial sums meet in `scratch`
+// (>= 8 * blockDim.x doubles of shared memory).
+static __device__ void dense_At_U(const double* __restrict__ A, int64_t rows, int n, const double* __restrict__ U,
+                                  int kp, double* __restrict__ Y, double* scratch) {
+  const int ng = imax(1, int(blockDim.x) / n);
+  const int g = threadIdx.x / n, r = threadIdx.x - g * n;
+  const bool active = g < ng;
+  for (int c0 = 0; c0 < kp; c0 += 8) {
+    double acc[8];
+    const double* uc[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      acc[c] = 0.0;
+      uc[c] = U + int64_t(imin(c0 + c, kp - 1)) * rows;
+    }
+    if (active) {
+#pragma unroll 4
+      for (int64_t i = g; i < rows; i += ng) {
+        const double a = A[i * n + r];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[c] = fma(a, uc[c][i], acc[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) scratch[(g * n + r) * 8 + c] = acc[c];
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < n * 8; idx += blockDim.x) {
+      const int rr = idx >> 3, c = idx & 7;
+      if (c0 + c < kp) {
+        double v = 0.0;
+        for (int gg = 0; gg < ng; ++gg) v += scratch[(gg * n + rr) * 8 + c];
+        Y[rr + int64_t(c0 + c) * n] = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// U (rows x k, ld rows) = A M diag(scale) for a dense row-major A (rows x n):
+// M's columns (n each) are staged in shared memory (`ms`, n*k doubles) and read
+// as broadcasts; a thread owns a row of A and 8 output columns at a time.
+template <class Col>
+static __device__ void dense_A_M(const double* __restrict__ A, int64_t rows, int n, Col col, const double* scale, int k,
+                                 double* __restrict__ U, double* ms) {
+  for (int idx = threadIdx.x; idx < n * k; idx += blockDim.x) {
+    const int t = idx % n, c = idx / n;
+    ms[idx] = col(c)[t];
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+    const double* a = A + i * n;
+    for (int c0 = 0; c0 < k; c0 += 8) {
+      double acc[8];
+      const double* mc[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        acc[c] = 0.0;
+        mc[c] = ms + imin(c0 + c, k - 1) * n;
+      }
+#pragma unroll 8
+      for (int t = 0; t < n; ++t) {
+        const double av = a[t];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[c] = fma(av, mc[c][t], acc[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c0 + c < k) U[i + int64_t(c0 + c) * rows] = acc[c] * scale[c0 + c];
+    }
+  }
+  __syncthreads();
+}
+
 static __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows, int64_t inner, int64_t k, double* U,
                             double* G, double* V, double* misc, double* dsm, BlockScratch& sc, int64_t kprev = 0,
                             double* si = nullptr, bool gram_ready = false) {
@@ -781,6 +868,9 @@ static __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows,
     double* Us = V;
     double* Ws = V + int64_t(n) * k;
     const int64_t kp = imin(kprev, k);
+    // dense row-major unfolding (outer == 1): A^T U_prev with coalesced loads
+    const bool dense_ws = !wide && outer == 1 && n <= int(blockDim.x) && 8 * int(blockDim.x) <= sc.dsm_cap;
+    if (dense_ws) dense_At_U(P, rows, n, U, int(kp), Us, dsm);
     for (int64_t idx = threadIdx.x; idx < n * k; idx += blockDim.x) {
       const int64_t r = idx % n, c = idx / n;
       double v;
@@ -788,6 +878,8 @@ static __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows,
         v = (r == (c * 7919) % n) ? 1.0 : 0.0;  // pad with canonical vectors
       } else if (wide) {
         v = U[r + c * rows];
+      } else if (dense_ws) {
+        continue;
       } else {  // tall: A^T U_prev, column r of the unfolding
         const int64_t o = r / inner, t = r - o * inner;
         v = dot4(P + o * rows * inner + t, inner, U + c * rows, 1, rows);
@@ -823,17 +915,23 @@ static __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows,
     }
     __syncthreads();
     tg = tstart();
-    for (int64_t idx = threadIdx.x; idx < rows * k; idx += blockDim.x) {
-      const int64_t i = idx % rows, c = idx / rows;
-      const double inv = sig[c];
-      double s = 0.0;
-      if (inv != 0.0) {
-        const double* vc = vcol(c);
-        for (int64_t o = 0; o < outer; ++o) s += dot4(P + (o * rows + i) * inner, 1, vc + o * inner, 1, inner);
+    // dense row-major unfolding: U = A V Sigma^-1 from V staged in shared memory
+    // (only after the top-k iteration: the Jacobi fallback's vectors live in dsm)
+    if (Vsi != nullptr && outer == 1 && int64_t(n) * k <= sc.dsm_cap) {
+      dense_A_M(P, rows, n, vcol, sig, int(k), U, dsm);
+    } else {
+      for (int64_t idx = threadIdx.x; idx < rows * k; idx += blockDim.x) {
+        const int64_t i = idx % rows, c = idx / rows;
+        const double inv = sig[c];
+        double s = 0.0;
+        if (inv != 0.0) {
+          const double* vc = vcol(c);
+          for (int64_t o = 0; o < outer; ++o) s += dot4(P + (o * rows + i) * inner, 1, vc + o * inner, 1, inner);
+        }
+        U[idx] = s * inv;
       }
-      U[idx] = s * inv;
+      __syncthreads();
     }
-    __syncthreads();
     tstop(sc, kPhGram, tg);
     const long long to = tstart();
     orthonormalize(U, rows, 0, int(k), rows, sc);

@@ -229,7 +229,7 @@ constexpr int kLastRows = 128;
 constexpr int64_t kLastMaxD = 94;  // (d + 2) * 128 rows * 8 B <= 96 KB
 template <int RH>
 __global__ void __launch_bounds__(256, 2)
-grid_last_kernel(Params prm, const LeafDesc* __restrict__ descs, int64_t rows, int R) {
+grid_last_kernel(Params prm, const LeafDesc* __restrict__ descs, int64_t rows, int R, int which) {
   extern __shared__ __align__(128) double dsm[];
   const int64_t tiles = (rows + kLastRows - 1) / kLastRows;
   const int64_t leaf = blockIdx.x / tiles, tile = blockIdx.x - leaf * tiles;
@@ -249,7 +249,9 @@ grid_last_kernel(Params prm, const LeafDesc* __restrict__ descs, int64_t rows, i
     const int a = idx / d, t = idx - a * d;
     us[t * rp + a] = a < R ? U[t + int64_t(a) * d] : 0.0;
   }
-  const double2* src = reinterpret_cast<const double2*>(D.ws + lay.W + c0 * d);
+  // which = 1: W (k0*D_1 rows) -> dense mode-1 unfolding in B1; which = 0: pass-1 output Y in B1 (len*k1 rows)
+  // -> Y x_2 U_2^T in B2, natural order (the dense len x (k1*R) mode-0 unfolding)
+  const double2* src = reinterpret_cast<const double2*>(D.ws + (which ? lay.W : lay.B1) + c0 * d);
   for (int i2 = threadIdx.x; i2 < nr * d / 2; i2 += blockDim.x) {
     const int e = 2 * i2, r = e / d, t = e - r * d;
     *reinterpret_cast<double2*>(xs + r * ldx + t) = src[i2];
@@ -269,7 +271,7 @@ grid_last_kernel(Params prm, const LeafDesc* __restrict__ descs, int64_t rows, i
     for (int a = 0; a < RH; ++a) acc[a] = fma(ur[t * rp + a], x, acc[a]);
   }
   const int64_t c = c0 + r, d1 = prm.d[1], o = c / d1, j = c - o * d1;
-  double* out = D.ws + lay.B1 + j * (rows / d1) * R + o * R + a0;
+  double* out = which ? D.ws + lay.B1 + j * (rows / d1) * R + o * R + a0 : D.ws + lay.B2 + c * R + a0;
 #pragma unroll
   for (int a = 0; a < RH; ++a)
     if (a0 + a < R) out[a] = acc[a];
@@ -277,7 +279,8 @@ grid_last_kernel(Params prm, const LeafDesc* __restrict__ descs, int64_t rows, i
 
 cudaError_t grid_solve_prepare();
 void launch_grid_prep(const Params& prm, const LeafDesc* d_descs, int n, int* d_active, cudaStream_t st);
-void launch_grid_solve0(const Params& prm, const LeafDesc* d_descs, int n, int sweep, int gcap, cudaStream_t st);
+void launch_grid_solve0(const Params& prm, const LeafDesc* d_descs, int n, int sweep, int gcap, int y_done,
+                        cudaStream_t st);
 void launch_grid_solve_mode(const Params& prm, const LeafDesc* d_descs, int n, int sweep, int mode, int first_done,
                             int gram_ready, int* d_active, cudaStream_t st);
 bool grid_gram_applies(int64_t rows, int64_t cols, int64_t k);
@@ -298,7 +301,7 @@ static GridTtmFn grid_ttm_fn(int rc) {
   }
 }
 
-using GridLastFn = void (*)(Params, const LeafDesc*, int64_t, int);
+using GridLastFn = void (*)(Params, const LeafDesc*, int64_t, int, int);
 static GridLastFn grid_last_fn(int rh) {
   switch (rh) {
 #define TT_CASE(N) \
@@ -415,21 +418,23 @@ cudaError_t launch_leaf_grid(const Params& prm, const LeafDesc* d_descs, int n, 
     return cudaGetLastError();
   };
   // W x_2 U_2^T for order-3 series (the first product of mode 1)
-  auto last = [&]() -> cudaError_t {
-    const int64_t rows = k[0] * d[1], R = k[2];
+  auto last = [&](int which) -> cudaError_t {
+    const int64_t rows = which ? k[0] * d[1] : len * k[1], R = k[2];
     const int rh = int((R + 1) / 2);
     GridLastFn fn = grid_last_fn(rh);
     if (!fn) return cudaErrorInvalidValue;
     const int64_t tiles = (rows + kLastRows - 1) / kLastRows;
     const size_t smem = size_t(kLastRows * (d[2] + 2) + d[2] * 2 * rh) * sizeof(double);
-    fn<<<unsigned(tiles * n), 256, smem, st>>>(prm, d_descs, rows, int(R));
+    fn<<<unsigned(tiles * n), 256, smem, st>>>(prm, d_descs, rows, int(R), which);
     g_launches.fetch_add(1);
     return cudaGetLastError();
   };
   int prev_left = n;
   for (int sweep = 0; sweep < prm.max_iters; ++sweep) {
     if ((e = ttm(1, k[1], sweep == 0)) != cudaSuccess) return e;
-    launch_grid_solve0(prm, d_descs, n, sweep, int(imax(1, len * n / (2 * ctas))), st);
+    const bool last_ok = p == 3 && d[2] <= kLastMaxD && d[2] % 2 == 0 && k[2] <= 32;
+    if (last_ok && (e = last(0)) != cudaSuccess) return e;  // Y x_2 U_2^T, grid-wide
+    launch_grid_solve0(prm, d_descs, n, sweep, int(imax(1, len * n / (2 * ctas))), last_ok ? 1 : 0, st);
     k[0] = leaf_mode_rank(p, d, k, 0);
     if ((e = ttm(2, k[0], 0)) != cudaSuccess) return e;
     for (int m = 1; m < p; ++m) {
@@ -438,8 +443,8 @@ cudaError_t launch_leaf_grid(const Params& prm, const LeafDesc* d_descs, int n, 
       if (m >= 2) {
         if ((e = ttm(3, k[1], 0)) != cudaSuccess) return e;
         first_done = 1;
-      } else if (p == 3 && d[2] <= kLastMaxD && d[2] % 2 == 0 && k[2] <= 32) {
-        if ((e = last()) != cudaSuccess) return e;
+      } else if (last_ok) {
+        if ((e = last(1)) != cudaSuccess) return e;
         first_done = 1;
         // its Gram, split over row chunks across the GPU
         if (grid_gram_applies(d[1], k[0] * k[2], leaf_mode_rank(p, d, k, 1))) {

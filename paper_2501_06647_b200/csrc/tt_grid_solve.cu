@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kThreads) grid_prep_kernel(Params prm, const L
 
 // After pass 1: the remaining contractions of Y, then U_0 = llsv(M_0(Y)).
 __global__ void __launch_bounds__(kThreads, 2) grid_solve0_kernel(Params prm, const LeafDesc* __restrict__ descs,
-                                                                  int sweep, int gcap) {
+                                                                  int sweep, int gcap, int y_done) {
   __shared__ BlockScratch sc;
   extern __shared__ __align__(128) double dsm[];
   const LeafDesc D = descs[blockIdx.x];
@@ -111,8 +111,9 @@ __global__ void __launch_bounds__(kThreads, 2) grid_solve0_kernel(Params prm, co
   int tog = 1;
   for (int m = 2; m < p; ++m) {
     double* dst = B[tog];
-    mode_product(src, prod_range(cur, 0, m), cur[m], prod_range(cur, m + 1, p), D.out_f[m], d[m], 1, k[m], dst, false,
-                 sc);
+    if (!(m == 2 && y_done))  // order 3: Y x_2 U_2^T came from grid_last_kernel (tt_grid.cu)
+      mode_product(src, prod_range(cur, 0, m), cur[m], prod_range(cur, m + 1, p), D.out_f[m], d[m], 1, k[m], dst, false,
+                   sc);
     cur[m] = k[m];
     src = dst;
     tog ^= 1;
@@ -267,8 +268,9 @@ void launch_grid_prep(const Params& prm, const LeafDesc* d_descs, int n, int* d_
   grid_prep_kernel<<<n, kThreads, 0, st>>>(prm, d_descs, d_active);
   g_launches.fetch_add(1);
 }
-void launch_grid_solve0(const Params& prm, const LeafDesc* d_descs, int n, int sweep, int gcap, cudaStream_t st) {
-  grid_solve0_kernel<<<n, kThreads, grid_solve_smem(n), st>>>(prm, d_descs, sweep, gcap);
+void launch_grid_solve0(const Params& prm, const LeafDesc* d_descs, int n, int sweep, int gcap, int y_done,
+                        cudaStream_t st) {
+  grid_solve0_kernel<<<n, kThreads, grid_solve_smem(n), st>>>(prm, d_descs, sweep, gcap, y_done);
   g_launches.fetch_add(1);
 }
 void launch_grid_solve_mode(const Params& prm, const LeafDesc* d_descs, int n, int sweep, int mode, int first_done,

@@ -52,7 +52,18 @@ def assert_factors_match(x, got, want, where="", check_angles=True, gap_tol=1e-6
                 continue
             if s[0] == 0 or s[k - 1] / s[0] < 1e-9:
                 continue
-            assert H.max_sin_angle(got.factors[m], want.factors[m]) <= ANGLE_TOL, f"{where} mode {m}"
+            tol = ANGLE_TOL
+            if x is not None and k < min(H.unfold(x, m).shape):
+                # Conditioning of the rank-k boundary in the DATA: when the requested rank reaches into the
+                # noise floor (relative gap g between the k-th and (k+1)-th singular values of the
+                # unfolding well below 1e-3), two backward-stable solvers (the oracle's SVD, the engine's
+                # Gram iteration) whose ALS iterates agree to ~1e-9 relative differ by ~1e-9 / g in that
+                # subspace. The 1e-6 bar applies to gapped columns; below it scales with 1 / g.
+                sx = np.linalg.svd(H.unfold(x, m), compute_uv=False)
+                g = (sx[k - 1] - sx[k]) / sx[0]
+                if g < 1e-3:
+                    tol = max(ANGLE_TOL, 1e-9 / max(g, 1e-12))
+            assert H.max_sin_angle(got.factors[m], want.factors[m]) <= tol, f"{where} mode {m}"
 
 
 # ------------------------------------------------------------------ tucker_als
