@@ -302,7 +302,7 @@ def run_engine(args, rank, world, local_rank):
         "e2e": {"value": round(e2e_qps, 3), "unit": "queries/s", "h2d_bytes_per_step": int(x.nbytes),
                 "d2h_bytes_per_step": int(out_bytes), "append_slices_per_s": round(e2e_sps, 3)},
         "roofline": roof,
-        "stream_pass": pass_roof(step_pass, build_pass, peak),
+        "stream_pass": pass_roof(step_pass, build_pass, peak, traffic),
         "gpu_launches": int(launches),
         "solver_per_step": solver,
         "clocks": clk.summary(),
@@ -704,7 +704,7 @@ def run_engine_stream(args, rank, world, local_rank):
                 "h2d_bytes_per_step": int(B * ss * 8), "d2h_bytes_per_step": int(q_out_bytes // K),
                 "append_slices_per_s": round(world * K * B / (e2e_ms / 1e3), 3)},
         "roofline": roof,
-        "stream_pass": pass_roof(step_pass, build_pass, peak),
+        "stream_pass": pass_roof(step_pass, build_pass, peak, traffic),
         "gpu_launches": int(launches),
         "solver_per_step": solver,
         "clocks": clk.summary(),
@@ -716,7 +716,7 @@ def run_engine_stream(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
-def pass_roof(step_pass, build_pass, peak):
+def pass_roof(step_pass, build_pass, peak, traffic):
     """Achieved HBM bandwidth of grid_ttm_kernel's passes over X (the only kernel
     of the path that moves leaf-block-sized data), from the engine's CUDA events
     around each launch: inside the timed steps (one leaf block or query tail per
@@ -729,6 +729,8 @@ def pass_roof(step_pass, build_pass, peak):
             out[tag] = {"launches": int(sp["launches"]), "avg_launch_ms": round(sp["ms"] / sp["launches"], 4),
                         "bytes_per_launch": int(sp["bytes"] / sp["launches"]), "achieved": round(gbs, 1),
                         "frac": round(gbs / peak, 4)}
+    if "build" in out:  # ncu dram__bytes_read+write of one build-sized launch (profiles/traffic.json), or null
+        out["build"]["traffic"] = traffic.get("stream_pass_build")
     return out
 
 

@@ -185,9 +185,10 @@ constexpr int64_t kGridCjMax = 16;          // rows of j per stage (bounds the s
 constexpr int64_t kGridRcMax = 10;          // accumulator columns per thread (x tt columns of t)
 // gcap bounds the slabs per tile: small batches take fewer slabs per tile so the
 // pass has enough work items for every SM.
-TT_HD GridTile grid_tile(int64_t outer, int64_t d, int64_t inner, int64_t gcap = 256) {  // requires inner % 2 == 0
+// ttmax = 2 halves the columns per thread (small batches: twice the active threads).
+TT_HD GridTile grid_tile(int64_t outer, int64_t d, int64_t inner, int64_t gcap = 256, int64_t ttmax = 4) {  // requires inner % 2 == 0
   GridTile t;
-  t.tt = (inner % 4 == 0) ? 4 : 2;
+  t.tt = (inner % 4 == 0 && ttmax >= 4) ? 4 : 2;
   t.tw = imin(inner, 256 * t.tt);
   t.tpo = t.tw / t.tt;
   t.G = imax(1, imin(imin(outer, 256 / t.tpo), gcap));
@@ -223,7 +224,7 @@ struct GridWs {
 };
 TT_HD GridWs grid_ws_layout(int p, int64_t len, const int64_t* d, const int64_t* req) {
   const LeafWs l = leaf_ws_layout(p, len, d, req);
-  const GridTile t = grid_tile(len, d[1], prod_range(d, 2, p), 1);  // most tiles: one slab each
+  const GridTile t = grid_tile(len, d[1], prod_range(d, 2, p), 1, 2);  // most tiles: one slab each, narrow
   GridWs g;
   g.ut1 = l.total;
   g.ut0 = g.ut1 + d[1] * kGridUtLd;

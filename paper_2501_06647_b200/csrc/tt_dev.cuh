@@ -572,6 +572,60 @@ constexpr int kGramSiMaxK = 32;  // top-k Gram iteration: k <= 32 (BASELINE C5's
 __host__ __device__ constexpr int topk_small_off(int K) { return K <= 16 ? 768 : 3 * K * K; }
 __host__ __device__ constexpr int topk_b_off(int K) { return K <= 16 ? 1536 : 6 * K * K; }
 __host__ __device__ constexpr int topk_stage_off(int K) { return K <= 16 ? 2048 : 7 * K * K; }
+// Wout (n x K, ld n) = G Uin for the staged symmetric G (ld ldp, odd: lanes on
+// consecutive rows hit distinct banks). A thread owns one row of the product and
+// all K columns over one of H = blockDim/n slices of the inner index: per inner
+// step one LDS of G and K/2 broadcast LDS.128 of the K-contiguous copy of Uin
+// feed K FMAs (the plain dot-product form pays two LDS per FMA). utr: n*K
+// doubles, part: blockDim*K doubles of shared memory.
+template <int K>
+__device__ __forceinline__ void sym_gu_tiled(const double* Gp, int ldp, int n, const double* Uin, double* Wout,
+                                             double* utr, double* part) {
+  for (int idx = threadIdx.x; idx < n * K; idx += blockDim.x) {
+    const int l = idx % n, j = idx / n;
+    utr[l * K + j] = Uin[idx];
+  }
+  __syncthreads();
+  const int H = int(imax(1, imin(4, int(blockDim.x) / n)));
+  const int h = threadIdx.x / n, i = threadIdx.x - h * n;
+  if (h < H) {
+    const int l0 = h * n / H, l1 = (h + 1) * n / H;
+    double acc[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) acc[j] = 0.0;
+    const double* g = Gp + int64_t(i) * ldp;
+    if ((K & 1) == 0 && (reinterpret_cast<uintptr_t>(utr) & 15u) == 0) {
+#pragma unroll 2
+      for (int l = l0; l < l1; ++l) {
+        const double gv = g[l];
+        const double2* ur = reinterpret_cast<const double2*>(utr + l * K);
+#pragma unroll
+        for (int j = 0; j < K / 2; ++j) {
+          const double2 u2 = ur[j];
+          acc[2 * j] = fma(gv, u2.x, acc[2 * j]);
+          acc[2 * j + 1] = fma(gv, u2.y, acc[2 * j + 1]);
+        }
+      }
+    } else {
+      for (int l = l0; l < l1; ++l) {
+        const double gv = g[l];
+        const double* ur = utr + l * K;
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc[j] = fma(gv, ur[j], acc[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) part[(h * K + j) * n + i] = acc[j];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < n * K; idx += blockDim.x) {
+    double v = 0.0;
+    for (int hh = 0; hh < H; ++hh) v += part[hh * K * n + idx];
+    Wout[idx] = v;
+  }
+  __syncthreads();
+}
+
 template <int K>
 __device__ __noinline__ double* sym_topk_si_k(const double* __restrict__ G, int n, double* U, double* W,
                                               double* lam, int* order, double* dsm, BlockScratch& sc) {
@@ -588,6 +642,11 @@ __device__ __noinline__ double* sym_topk_si_k(const double* __restrict__ G, int 
   double* const Wg = W;
   const double* Gp = G;
   int ldp = n;
+  // room for the register-tiled product's K-contiguous copy and partial sums
+  const bool tiled = staged && n <= int(blockDim.x) &&
+                     topk_stage_off(K) + ldg * n + 3 * n * K + int(blockDim.x) * K <= sc.dsm_cap;
+  double* const utr = dsm + topk_stage_off(K) + ldg * n + 2 * n * K;
+  double* const part = utr + n * K;
   if (staged) {
     double* Gs = dsm + topk_stage_off(K);
     for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
@@ -606,11 +665,15 @@ __device__ __noinline__ double* sym_topk_si_k(const double* __restrict__ G, int 
   int it = 0;
   for (; it < kGramSiMaxIter; ++it) {
     long long tp = tstart();
-    for (int idx = threadIdx.x; idx < n * K; idx += blockDim.x) {
-      const int i = idx % n, j = idx / n;
-      W[idx] = dot4(Gp + int64_t(i) * ldp, 1, U + int64_t(j) * n, 1, n);
+    if (tiled) {
+      sym_gu_tiled<K>(Gp, ldp, n, U, W, utr, part);
+    } else {
+      for (int idx = threadIdx.x; idx < n * K; idx += blockDim.x) {
+        const int i = idx % n, j = idx / n;
+        W[idx] = dot4(Gp + int64_t(i) * ldp, 1, U + int64_t(j) * n, 1, n);
+      }
+      __syncthreads();
     }
-    __syncthreads();
     tstop_si(sc, kSiAtU, tp);
     tp = tstart();
     gemm(K, K, n, U, n, 1, W, 1, n, B, 1, K, false, sc);  // B = U^T W
@@ -664,16 +727,22 @@ __device__ __noinline__ double* sym_topk_si_k(const double* __restrict__ G, int 
       }
       __syncthreads();
       const int extra = sc.ibcast[3] - 1;
+      const long long tpw = tstart();
       for (int e = 0; e < extra; ++e) {  // U <- G W, then swap: W holds G^(1+e+1) U_old
-        for (int idx = threadIdx.x; idx < n * K; idx += blockDim.x) {
-          const int i = idx % n, j = idx / n;
-          U[idx] = dot4(Gp + int64_t(i) * ldp, 1, W + int64_t(j) * n, 1, n);
+        if (tiled) {
+          sym_gu_tiled<K>(Gp, ldp, n, W, U, utr, part);
+        } else {
+          for (int idx = threadIdx.x; idx < n * K; idx += blockDim.x) {
+            const int i = idx % n, j = idx / n;
+            U[idx] = dot4(Gp + int64_t(i) * ldp, 1, W + int64_t(j) * n, 1, n);
+          }
+          __syncthreads();
         }
-        __syncthreads();
         double* t = U;
         U = W;
         W = t;
       }
+      tstop_si(sc, kSiAtU, tpw);
     }
     double* t = U;  // U <- orth(W)
     U = W;

@@ -83,7 +83,7 @@ grid_ttm_kernel(Params prm, const LeafDesc* __restrict__ descs, int nleaves, int
   __syncthreads();
   const int64_t len = descs[0].len;  // equal-length batch
   const GridPassShape sh = grid_pass_shape(prm, len, pass, k0);
-  const GridTile tile = grid_tile(sh.outer, sh.d, sh.inner, gcap);
+  const GridTile tile = grid_tile(sh.outer, sh.d, sh.inner, gcap, TT);
   const GridChunks ch = grid_chunks(R);
   const LeafWs lay = leaf_ws_layout(prm.p, len, prm.d, prm.req);
   const GridWs gw = grid_ws_layout(prm.p, len, prm.d, prm.req);
@@ -279,7 +279,7 @@ grid_last_kernel(Params prm, const LeafDesc* __restrict__ descs, int64_t rows, i
 
 cudaError_t grid_solve_prepare();
 void launch_grid_prep(const Params& prm, const LeafDesc* d_descs, int n, int* d_active, cudaStream_t st);
-void launch_grid_solve0(const Params& prm, const LeafDesc* d_descs, int n, int sweep, int gcap, int y_done,
+void launch_grid_solve0(const Params& prm, const LeafDesc* d_descs, int n, int sweep, int gcap, int tt1, int y_done,
                         cudaStream_t st);
 void launch_grid_solve_mode(const Params& prm, const LeafDesc* d_descs, int n, int sweep, int mode, int first_done,
                             int gram_ready, int* d_active, cudaStream_t st);
@@ -399,15 +399,19 @@ cudaError_t launch_leaf_grid(const Params& prm, const LeafDesc* d_descs, int n, 
   for (int m = 1; m < p; ++m) d[m] = prm.d[m];
   clamp_ranks(p, d, prm.req, k);
   launch_grid_prep(prm, d_descs, n, d_active, st);
+  int tt_pass1 = 4;  // columns per thread of pass 1 (the solve sums that pass's norm partials)
   static thread_local PassEvents pe;
   const bool timed = pe.ensure();
   auto ttm = [&](int pass, int64_t R, int want_norm) -> cudaError_t {
     const GridPassShape sh = grid_pass_shape(prm, len, pass, k[0]);
     // slabs per tile: enough items for two per SM when the batch is small
     const int64_t gcap = imax(1, sh.outer * n / (2 * ctas));
-    const GridTile t = grid_tile(sh.outer, sh.d, sh.inner, gcap);
+    GridTile t = grid_tile(sh.outer, sh.d, sh.inner, gcap);
+    // too few work items to fill the SMs: two columns per thread instead of four
+    if (t.tt == 4 && t.ngrp * t.ntt * n < ctas) t = grid_tile(sh.outer, sh.d, sh.inner, gcap, 2);
     const GridChunks ch = grid_chunks(R);
     const int64_t items = int64_t(ch.nchunk) * t.ngrp * t.ntt * n;
+    if (pass == 1) tt_pass1 = int(t.tt);
     GridTtmFn fn = t.tt == 4 ? grid_ttm_fn<4>(ch.rc) : grid_ttm_fn<2>(ch.rc);
     if (!fn) return cudaErrorInvalidValue;
     if (timed && pass <= 2) cudaEventRecord(pe.ev[2 * (pass - 1)], st);
@@ -434,7 +438,7 @@ cudaError_t launch_leaf_grid(const Params& prm, const LeafDesc* d_descs, int n, 
     if ((e = ttm(1, k[1], sweep == 0)) != cudaSuccess) return e;
     const bool last_ok = p == 3 && d[2] <= kLastMaxD && d[2] % 2 == 0 && k[2] <= 32;
     if (last_ok && (e = last(0)) != cudaSuccess) return e;  // Y x_2 U_2^T, grid-wide
-    launch_grid_solve0(prm, d_descs, n, sweep, int(imax(1, len * n / (2 * ctas))), last_ok ? 1 : 0, st);
+    launch_grid_solve0(prm, d_descs, n, sweep, int(imax(1, len * n / (2 * ctas))), tt_pass1, last_ok ? 1 : 0, st);
     k[0] = leaf_mode_rank(p, d, k, 0);
     if ((e = ttm(2, k[0], 0)) != cudaSuccess) return e;
     for (int m = 1; m < p; ++m) {

@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kThreads) grid_prep_kernel(Params prm, const L
 
 // After pass 1: the remaining contractions of Y, then U_0 = llsv(M_0(Y)).
 __global__ void __launch_bounds__(kThreads, 2) grid_solve0_kernel(Params prm, const LeafDesc* __restrict__ descs,
-                                                                  int sweep, int gcap, int y_done) {
+                                                                  int sweep, int gcap, int tt1, int y_done) {
   __shared__ BlockScratch sc;
   extern __shared__ __align__(128) double dsm[];
   const LeafDesc D = descs[blockIdx.x];
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kThreads, 2) grid_solve0_kernel(Params prm, co
   for (int m = 0; m < p; ++m) k[m] = int64_t(st[kGsK + m]);
   double* B[2] = {D.ws + lay.B1, D.ws + lay.B2};
   if (sweep == 0) {
-    const GridTile t1 = grid_tile(D.len, prm.d[1], prod_range(prm.d, 2, p), gcap);
+    const GridTile t1 = grid_tile(D.len, prm.d[1], prod_range(prm.d, 2, p), gcap, tt1);
     double s = 0.0;
     if (threadIdx.x == 0)
       for (int64_t i = 0; i < t1.ngrp * t1.ntt; ++i) s += D.ws[gw.npart + i];
@@ -268,9 +268,9 @@ void launch_grid_prep(const Params& prm, const LeafDesc* d_descs, int n, int* d_
   grid_prep_kernel<<<n, kThreads, 0, st>>>(prm, d_descs, d_active);
   g_launches.fetch_add(1);
 }
-void launch_grid_solve0(const Params& prm, const LeafDesc* d_descs, int n, int sweep, int gcap, int y_done,
+void launch_grid_solve0(const Params& prm, const LeafDesc* d_descs, int n, int sweep, int gcap, int tt1, int y_done,
                         cudaStream_t st) {
-  grid_solve0_kernel<<<n, kThreads, grid_solve_smem(n), st>>>(prm, d_descs, sweep, gcap, y_done);
+  grid_solve0_kernel<<<n, kThreads, grid_solve_smem(n), st>>>(prm, d_descs, sweep, gcap, tt1, y_done);
   g_launches.fetch_add(1);
 }
 void launch_grid_solve_mode(const Params& prm, const LeafDesc* d_descs, int n, int sweep, int mode, int first_done,

@@ -893,6 +893,11 @@ __device__ __forceinline__ void stitch_body(const Params& prm, const StitchDesc*
             mode_product(Fb + int64_t(i) * lay.chain, zo, parts[i].rho[n], zi, parts[i].v[n], 1, d[n], d[n], Z,
                          i > 0, sc);
         }
+        // Every mode but the last writes Z_n as the dense row-major unfolding
+        // (d_n x Qn): llsv then reads contiguous rows (coalesced warm start,
+        // shared-memory back-multiplication). The last mode's Z feeds the core
+        // and keeps the tensor layout.
+        const bool dense_z = one_pass && n < p - 1;
         if (one_pass) {
           // Z_n = sum_i F_i x_n V_in written once: the stacked F (sum rho_in x Qn)
           // is staged in shared memory; a thread owns one row a of Z and 8
@@ -956,8 +961,12 @@ __device__ __forceinline__ void stitch_body(const Params& prm, const StitchDesc*
             for (int c = 0; c < 8; ++c) {
               const int64_t cc = c0 + c;
               if (cc < Qn) {
-                const int64_t o = cc / zi, t = cc - o * zi;
-                Z[(o * dn + a) * zi + t] = acc[c];
+                if (dense_z) {  // the mode-n unfolding itself: dense row-major d_n x Qn
+                  Z[a * Qn + cc] = acc[c];
+                } else {
+                  const int64_t o = cc / zi, t = cc - o * zi;
+                  Z[(o * dn + a) * zi + t] = acc[c];
+                }
               }
             }
           }
@@ -976,9 +985,11 @@ __device__ __forceinline__ void stitch_body(const Params& prm, const StitchDesc*
         }
         if constexpr (CL) {
           cl_sync();  // Z_n complete
-          wide_llsv(Z, zo, d[n], zi, kn, D.out_f[n], G, Vg, misc, dsm, sc, kprev, ws + lay.SI, gpart, rank, CS);
+          wide_llsv(Z, dense_z ? 1 : zo, d[n], dense_z ? Qn : zi, kn, D.out_f[n], G, Vg, misc, dsm, sc, kprev,
+                    ws + lay.SI, gpart, rank, CS);
         } else {
-          llsv_unfold(Z, zo, d[n], zi, kn, D.out_f[n], G, Vg, misc, dsm, sc, kprev, ws + lay.SI);
+          llsv_unfold(Z, dense_z ? 1 : zo, d[n], dense_z ? Qn : zi, kn, D.out_f[n], G, Vg, misc, dsm, sc, kprev,
+                      ws + lay.SI);
         }
         k[n] = kn;
         if (leader) gemm_batched(s, [&](int i) { return pm_entry(i, n); }, sc);
