@@ -349,6 +349,65 @@ static __device__ void chol_inv_warp(const double* G, int k, double* L, double* 
   }
 }
 
+// The same factorisation for K <= 16, register-resident: lane i holds row i of
+// G; the right-looking update takes the pivot and the column entries from the
+// owning lanes by shuffle, and L^{-1} is formed column-per-lane by forward
+// substitution over shuffled entries of L. No shared-memory round trips, one
+// rsqrt per column on the serial chain (~2k cycles at K = 10 against ~7k for
+// chol_inv_warp). Writes Linv only (col-major, lower; the strict upper part 0).
+template <int K>
+static __device__ void chol_inv_warp_reg(const double* G, double* Linv, BlockScratch& sc) {
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  const unsigned full = 0xffffffffu;
+  const int row = lane < K ? lane : K - 1;
+  double g[K], invd[K];
+  double mydiag = 0.0;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    g[j] = G[row + j * K];
+    if (j == row) mydiag = g[j];
+  }
+  double dmax = mydiag;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(full, dmax, o));
+  bool ok = dmax > 0.0;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const double d = __shfl_sync(full, g[j], j);  // the updated pivot (uniform)
+    // pivots below 1e-14 * dmax: rank-deficient Gram, the caller falls back
+    if (!(d > 1e-14 * dmax)) ok = false;
+    const double inv = rsqrt(d);
+    invd[j] = inv;
+    const double lij = (lane == j) ? d * inv : g[j] * inv;  // L(lane, j), meaningful for lane >= j
+    g[j] = lij;
+#pragma unroll
+    for (int m = j + 1; m < K; ++m) {
+      const double lmj = __shfl_sync(full, lij, m);
+      g[m] = fma(-lij, lmj, g[m]);  // meaningful for lane >= m
+    }
+  }
+  if (!ok) {
+    if (lane == 0) sc.ibcast[2] = 1;
+    return;
+  }
+  double x[K];  // column `lane` of L^{-1}
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    double v = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+    for (int l = 0; l < i; ++l) {
+      const double lil = __shfl_sync(full, g[l], i);  // L(i, l)
+      v = fma(-lil, x[l], v);                         // x[l] = 0 above the diagonal (l < lane)
+    }
+    x[i] = (i >= lane) ? v * invd[i] : 0.0;
+  }
+  if (lane < K) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) Linv[i + lane * K] = x[i];
+  }
+}
+
 // W (rows x K, ld rows) <- W L^{-T}, where W^T W = L L^T (one CholeskyQR pass).
 template <int K>
 __device__ __noinline__ bool cholqr_pass_k(double* W, int64_t rows, double* small, BlockScratch& sc) {
@@ -358,7 +417,10 @@ __device__ __noinline__ bool cholqr_pass_k(double* W, int64_t rows, double* smal
   gram_tall(W, rows, rows, K, G);
   if (threadIdx.x == 0) sc.ibcast[2] = 0;
   __syncthreads();
-  chol_inv_warp(G, K, L, Li, sc);
+  if constexpr (K <= 16)
+    chol_inv_warp_reg<K>(G, Li, sc);
+  else
+    chol_inv_warp(G, K, L, Li, sc);
   __syncthreads();
   if (sc.ibcast[2]) return false;
   for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) {
@@ -579,8 +641,8 @@ __host__ __device__ constexpr int topk_stage_off(int K) { return K <= 16 ? 2048 
 // feed K FMAs (the plain dot-product form pays two LDS per FMA). utr: n*K
 // doubles, part: blockDim*K doubles of shared memory.
 template <int K>
-__device__ __forceinline__ void sym_gu_tiled(const double* Gp, int ldp, int n, const double* Uin, double* Wout,
-                                             double* utr, double* part) {
+__device__ __noinline__ void sym_gu_tiled(const double* Gp, int ldp, int n, const double* Uin, double* Wout,
+                                          double* utr, double* part) {
   for (int idx = threadIdx.x; idx < n * K; idx += blockDim.x) {
     const int l = idx % n, j = idx / n;
     utr[l * K + j] = Uin[idx];
@@ -643,7 +705,8 @@ __device__ __noinline__ double* sym_topk_si_k(const double* __restrict__ G, int 
   const double* Gp = G;
   int ldp = n;
   // room for the register-tiled product's K-contiguous copy and partial sums
-  const bool tiled = staged && n <= int(blockDim.x) &&
+  // (k <= 16: one out-of-line copy per K keeps the build time in check)
+  const bool tiled = K <= 16 && staged && n <= int(blockDim.x) &&
                      topk_stage_off(K) + ldg * n + 3 * n * K + int(blockDim.x) * K <= sc.dsm_cap;
   double* const utr = dsm + topk_stage_off(K) + ldg * n + 2 * n * K;
   double* const part = utr + n * K;
@@ -666,7 +729,7 @@ __device__ __noinline__ double* sym_topk_si_k(const double* __restrict__ G, int 
   for (; it < kGramSiMaxIter; ++it) {
     long long tp = tstart();
     if (tiled) {
-      sym_gu_tiled<K>(Gp, ldp, n, U, W, utr, part);
+      if constexpr (K <= 16) sym_gu_tiled<K>(Gp, ldp, n, U, W, utr, part);
     } else {
       for (int idx = threadIdx.x; idx < n * K; idx += blockDim.x) {
         const int i = idx % n, j = idx / n;
@@ -730,7 +793,7 @@ __device__ __noinline__ double* sym_topk_si_k(const double* __restrict__ G, int 
       const long long tpw = tstart();
       for (int e = 0; e < extra; ++e) {  // U <- G W, then swap: W holds G^(1+e+1) U_old
         if (tiled) {
-          sym_gu_tiled<K>(Gp, ldp, n, W, U, utr, part);
+          if constexpr (K <= 16) sym_gu_tiled<K>(Gp, ldp, n, W, U, utr, part);
         } else {
           for (int idx = threadIdx.x; idx < n * K; idx += blockDim.x) {
             const int i = idx % n, j = idx / n;

@@ -20,6 +20,8 @@ def _run(tool, timeout):
            os.path.join(ROOT, "tools", "sanitize_smoke.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
     out = r.stdout + r.stderr
+    if "compute-sanitizer is closed" in out:  # pools where the tool is disabled answer with this notice
+        pytest.skip("compute-sanitizer is closed on this GPU pool")
     assert r.returncode == 0 and "sanitize smoke ok" in out, out[-4000:]
     assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
 
