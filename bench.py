@@ -196,6 +196,7 @@ def run_engine(args, rank, world, local_rank):
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = eng.kernel_launches()
+    sp0 = eng.stream_pass_stats()
     stats0 = eng.solver_stats()
     t_app = t_q = t_leaf = t_stitch_build = t_stitch_q = 0.0
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -212,6 +213,8 @@ def run_engine(args, rank, world, local_rank):
         ev1.record()
         torch.cuda.synchronize()
     launches = eng.kernel_launches() - launches0
+    sp1 = eng.stream_pass_stats()
+    step_pass = {k: sp1[k] - sp0[k] for k in sp0}
     stats1 = eng.solver_stats()
     solver = {k: (stats1[k] - stats0[k]) / args.steps for k in ("problems", "als_sweeps", "eig_calls", "jacobi_sweeps",
                                                                 "subspace_ok", "subspace_fallback", "subspace_iters")}
@@ -302,7 +305,7 @@ def run_engine(args, rank, world, local_rank):
         "e2e": {"value": round(e2e_qps, 3), "unit": "queries/s", "h2d_bytes_per_step": int(x.nbytes),
                 "d2h_bytes_per_step": int(out_bytes), "append_slices_per_s": round(e2e_sps, 3)},
         "roofline": roof,
-        "stream_pass": pass_roof(step_pass, build_pass, peak, traffic),
+        "stream_pass": pass_roof(step_pass, {"launches": 0, "ms": 0.0, "bytes": 0.0}, peak, {}),
         "gpu_launches": int(launches),
         "solver_per_step": solver,
         "clocks": clk.summary(),

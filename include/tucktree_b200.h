@@ -136,7 +136,10 @@ void tt_tree_destroy(tt_tree* tree);
 /* StreamSegmentTree::append, n slices at once (one slice = prod D doubles,
  * row-major). Burst appends are processed level-synchronously: every new leaf
  * block is decomposed in one batched launch, then every completed parent,
- * level by level — result-identical to n sequential appends.  sst.hpp:64-67 */
+ * level by level — result-identical to n sequential appends.  sst.hpp:64-67
+ * TT_MEM_DEVICE sources are read on the engine's own non-blocking stream: the
+ * bytes must be complete (synchronise the stream that produced them) before
+ * the call; the call returns after the engine has finished reading them.   */
 tt_status tt_append(tt_tree* tree, const double* slices, int64_t n, tt_mem where);
 
 /* Empties the tree (timespan 0, no nodes) but keeps its device buffers and

@@ -175,6 +175,10 @@ struct DevBuf {
     bytes = 0;
     const size_t nb = std::max<size_t>(b + b / 4, 256);  // grow geometrically
     cuda_check(cudaMalloc(&p, nb), "cudaMalloc");
+    if (std::getenv("TT_POISON")) {  // debugging: NaN-fill fresh device buffers
+      cudaMemset(p, 0xFF, nb);
+      cudaDeviceSynchronize();
+    }
     bytes = nb;
   }
   template <class T>
@@ -224,6 +228,10 @@ struct Arena {
       const size_t cb = std::max(kChunk, b);
       void* c = nullptr;
       cuda_check(cudaMalloc(&c, cb), "cudaMalloc(arena)");
+      if (std::getenv("TT_POISON")) {
+        cudaMemset(c, 0xFF, cb);
+        cudaDeviceSynchronize();
+      }
       chunks.emplace_back(c, cb);
       ci = chunks.size() - 1;
       cur = static_cast<char*>(c);
@@ -378,6 +386,10 @@ std::vector<ProblemStatus> run_leaf_batch(Exec& ex, const Params& prm, std::vect
   size_t ws_total = 0;
   for (Index w : wsz) ws_total += static_cast<size_t>(w);
   ex.d_ws.ensure(ws_total * sizeof(double));
+  // TT_POISON=1 (debugging): fill the workspace with NaNs so that a read of a
+  // region no kernel has written shows up in the results
+  if (std::getenv("TT_POISON"))
+    cuda_check(cudaMemsetAsync(ex.d_ws.p, 0xFF, ws_total * sizeof(double), ex.stream), "workspace poison");
   ex.d_status.ensure((size_t(n) * kStatusInts + size_t(prm.max_iters)) * sizeof(int32_t));
   ex.d_obj.ensure(size_t(n) * prm.max_iters * sizeof(double));
   size_t off = 0;

@@ -159,4 +159,7 @@ def generate_torch(w: Workload, seed: int = 0, T: int | None = None, device="cud
             blk += 0.05 * torch.randn(blk.shape, **kw)
         elif w.name == "c5":
             blk += (0.01 * nrm / np.sqrt(N)) * torch.randn(blk.shape, **kw)
+    # The engine reads device sources on its own (non-blocking) stream: the bytes
+    # must be complete before a caller hands x.data_ptr() to tt_append.
+    torch.cuda.synchronize(x.device)
     return x
