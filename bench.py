@@ -263,21 +263,16 @@ def run_engine(args, rank, world, local_rank):
     leaf_gbs = leaf_bytes * K / (t_leaf / 1e3) / 1e9
     qbytes = query_algorithmic_bytes(w, trees[-1], ranges)
     q_gbs = qbytes * K / (t_stitch_q / 1e3) / 1e9
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof))
-        except Exception:
-            traffic = None
+    traffic = load_traffic(w.name)  # ncu captures are keyed by workload; null without one for this workload
     if t_stitch_q >= t_leaf:
         roof = {"kernel": "stitch_als_kernel (range-query batch)", "bound": "hbm", "achieved": round(q_gbs, 3),
                 "peak": peak, "unit": "GB/s", "frac": round(q_gbs / peak, 5),
-                "traffic": (traffic or {}).get("stitch_als_kernel"),
+                "traffic": traffic.get("stitch"),
                 "algorithmic_bytes_per_launch": qbytes, "peak_kind": peak_kind}
     else:
-        roof = {"kernel": "leaf_als_kernel", "bound": "hbm", "achieved": round(leaf_gbs, 3), "peak": peak,
-                "unit": "GB/s", "frac": round(leaf_gbs / peak, 5), "traffic": (traffic or {}).get("leaf_als_kernel"),
+        roof = {"kernel": "leaf ALS of the build (grid_ttm passes + per-leaf solver kernels)", "bound": "hbm",
+                "achieved": round(leaf_gbs, 3), "peak": peak,
+                "unit": "GB/s", "frac": round(leaf_gbs / peak, 5), "traffic": traffic.get("leaf"),
                 "algorithmic_bytes_per_launch": leaf_bytes, "peak_kind": peak_kind}
     line = {
         "metric": "range_tucker_queries_per_s",

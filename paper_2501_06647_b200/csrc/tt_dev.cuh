@@ -355,8 +355,11 @@ static __device__ void chol_inv_warp(const double* G, int k, double* L, double* 
 // substitution over shuffled entries of L. No shared-memory round trips, one
 // rsqrt per column on the serial chain (~2k cycles at K = 10 against ~7k for
 // chol_inv_warp). Writes Linv only (col-major, lower; the strict upper part 0).
+// rel_pivot > 0 also fails the factorisation when a pivot drops below
+// rel_pivot * G(j, j): column j lost more than that share of its squared norm
+// against the earlier columns (CGS2's collapse test with rel_pivot = 0.25).
 template <int K>
-static __device__ void chol_inv_warp_reg(const double* G, double* Linv, BlockScratch& sc) {
+static __device__ void chol_inv_warp_reg(const double* G, double* Linv, BlockScratch& sc, double rel_pivot = 0.0) {
   if (threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
   const unsigned full = 0xffffffffu;
@@ -375,8 +378,9 @@ static __device__ void chol_inv_warp_reg(const double* G, double* Linv, BlockScr
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     const double d = __shfl_sync(full, g[j], j);  // the updated pivot (uniform)
+    const double g0 = __shfl_sync(full, mydiag, j);  // the original diagonal entry
     // pivots below 1e-14 * dmax: rank-deficient Gram, the caller falls back
-    if (!(d > 1e-14 * dmax)) ok = false;
+    if (!(d > 1e-14 * dmax) || !(d > rel_pivot * g0)) ok = false;
     const double inv = rsqrt(d);
     invd[j] = inv;
     const double lij = (lane == j) ? d * inv : g[j] * inv;  // L(lane, j), meaningful for lane >= j
@@ -410,7 +414,8 @@ static __device__ void chol_inv_warp_reg(const double* G, double* Linv, BlockScr
 
 // W (rows x K, ld rows) <- W L^{-T}, where W^T W = L L^T (one CholeskyQR pass).
 template <int K>
-__device__ __noinline__ bool cholqr_pass_k(double* W, int64_t rows, double* small, BlockScratch& sc) {
+__device__ __noinline__ bool cholqr_pass_k(double* W, int64_t rows, double* small, BlockScratch& sc,
+                                           double rel_pivot = 0.0) {
   double* G = small;
   double* L = small + K * K;
   double* Li = small + 2 * K * K;
@@ -418,7 +423,7 @@ __device__ __noinline__ bool cholqr_pass_k(double* W, int64_t rows, double* smal
   if (threadIdx.x == 0) sc.ibcast[2] = 0;
   __syncthreads();
   if constexpr (K <= 16)
-    chol_inv_warp_reg<K>(G, Li, sc);
+    chol_inv_warp_reg<K>(G, Li, sc, rel_pivot);
   else
     chol_inv_warp(G, K, L, Li, sc);
   __syncthreads();
@@ -876,6 +881,22 @@ __device__ __forceinline__ bool llsv_uses_subspace(int64_t rows, int64_t cols, i
   return si != nullptr && kprev > 0 && rows > cols && cols >= 2 * k && cols * k <= kSiMaxYK && k <= kSiMaxK &&
          si_base() + kSiMaxYK + 5 * k * k + 256 <= sc.dsm_cap;
 }
+// Two CholeskyQR passes on W (rows x k, ld rows), k <= 16; false on a breakdown
+// or when a column collapses against the earlier ones (CGS2's completion case;
+// W is then unchanged or still spans the same space). small: 3 k^2 doubles.
+static __device__ bool cholqr2(double* W, int64_t rows, int k, double* small, BlockScratch& sc) {
+  switch (k) {
+#define TT_CASE(N) \
+  case N:          \
+    return cholqr_pass_k<N>(W, rows, small, sc, 0.25) && cholqr_pass_k<N>(W, rows, small, sc);
+    TT_CASE(1) TT_CASE(2) TT_CASE(3) TT_CASE(4) TT_CASE(5) TT_CASE(6) TT_CASE(7) TT_CASE(8)
+    TT_CASE(9) TT_CASE(10) TT_CASE(11) TT_CASE(12) TT_CASE(13) TT_CASE(14) TT_CASE(15) TT_CASE(16)
+#undef TT_CASE
+    default:
+      return false;
+  }
+}
+
 // Y (n x kp, ld n) = A^T U for a dense row-major A (rows x n, n <= blockDim.x)
 // and U (rows x kp, ld rows): a thread owns one column of A in one of
 // blockDim.x / n row groups and 8 columns of U at a time (coalesced loads of
@@ -1066,7 +1087,12 @@ static __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows,
     }
     tstop(sc, kPhGram, tg);
     const long long to = tstart();
-    orthonormalize(U, rows, 0, int(k), rows, sc);
+    // U = A V Sigma^-1 is orthonormal to ~1e-10 already: CholeskyQR2 gives the same
+    // Q as Gram-Schmidt (the QR factor with positive diagonal is unique) in two
+    // short passes instead of ~4 block reductions per column; a rank-deficient U
+    // (zeroed columns) breaks the Cholesky down and takes CGS2 with completion.
+    if (!(k <= 16 && 3 * k * k <= sc.dsm_cap && cholqr2(U, rows, int(k), dsm, sc)))
+      orthonormalize(U, rows, 0, int(k), rows, sc);
     tstop(sc, kPhOrtho, to);
   }
   const long long ts = tstart();

@@ -371,12 +371,20 @@ std::vector<ProblemStatus> run_leaf_batch(Exec& ex, const Params& prm, std::vect
   // Batches of equal-length, 16-byte-aligned blocks: the grid-wide phase
   // kernels (tt_grid.cu) stream X across the whole GPU. TT_GRID=0 disables the
   // path, 1 keeps the cluster kernel for small batches, 2 (default) takes it
-  // for every eligible batch (A/B measurement).
+  // for every eligible batch but wide batches of small blocks, 3 for those too
+  // (A/B measurement, tests).
   int grid_mode = 2;
   if (const char* e = std::getenv("TT_GRID")) grid_mode = std::atoi(e);
   bool grid = grid_mode > 0 && (grid_mode >= 2 || !wide) && leaf_grid_ok(prm, descs[0].len);
   for (int i = 0; grid && i < n; ++i)
     grid = descs[i].len == descs[0].len && (reinterpret_cast<uintptr_t>(descs[i].x) & 15u) == 0;
+  // Wide batches of small blocks (C1: 0.26 MB, C2: 2.3 MB per leaf) are bound by
+  // the per-leaf solvers, not by the passes over X: one CTA per leaf keeps each
+  // leaf's working set in one SM's L1 and measured 10% faster there. TT_GRID=3
+  // takes the grid path regardless (tests).
+  if (grid && !wide && grid_mode < 3 &&
+      double(descs[0].len) * double(prod_range(prm.d, 1, prm.p)) * sizeof(double) < 4.0e6)
+    grid = false;
   if (grid) wide = false;
   std::vector<Index> wsz(ws_sizes);
   if (wide)  // + the per-CTA partial Gram slots of the cluster kernel

@@ -13,6 +13,19 @@ from tests.test_gpu_parity import E, _compare_trees, _ranges, _series  # noqa: F
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _force_grid_path():
+    """TT_GRID=3: the grid-wide path for every eligible batch, including the wide
+    batches of small blocks the default heuristic leaves to the one-CTA kernel."""
+    old = os.environ.get("TT_GRID")
+    os.environ["TT_GRID"] = "3"
+    yield
+    if old is None:
+        os.environ.pop("TT_GRID", None)
+    else:
+        os.environ["TT_GRID"] = old
+
+
 @pytest.mark.parametrize("shape,true_r,ranks,B,noise,seed", [
     ((40 * 16, 20, 12), (4, 4, 4), (4, 4, 4), 16, 0.1, 1),       # TT=4 on both passes, 40 leaves
     ((32 * 8, 14, 6), (3, 3, 3), (5, 4, 3), 8, 0.2, 2),          # inner 6: TT=2 first pass, ragged tiles
@@ -31,14 +44,14 @@ def test_grid_matches_one_cta_kernel(E):
     # same build through both leaf paths: sweep counts identical, factors to rounding
     series = _series((48 * 16, 36, 20), (5, 5, 5), 0.3, 9)
     trees = []
-    for flag in ("1", "0"):
+    for flag in ("3", "0"):
         os.environ["TT_GRID"] = flag
-        try:
-            t = E.StreamSegmentTree(series.shape[1:], (5, 5, 5), leaf_block=16)
-            t.append(series)
-        finally:
-            os.environ.pop("TT_GRID", None)
+        t = E.StreamSegmentTree(series.shape[1:], (5, 5, 5), leaf_block=16)
+        l0 = E.kernel_launches()
+        t.append(series)
         trees.append(t)
+        if flag == "3":  # the phase kernels ran: far more launches than one leaf launch + the stitch levels
+            assert E.kernel_launches() - l0 > 20
     a, b = trees
     for v in a.nodes():
         if not v.has_decomposition:
