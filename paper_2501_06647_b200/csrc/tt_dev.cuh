@@ -349,7 +349,12 @@ static __device__ void chol_inv_warp(const double* G, int k, double* L, double* 
   }
 }
 
-// The same factorisation for K <= 16, register-resident: lane i holds row i of
+// Ranks up to kRegK (the BASELINE configs C1-C4 use 4..10) get the fully unrolled
+// register-resident solver pieces below; larger ranks keep the shared-memory
+// forms (the unrolled code grows with K^2 and so does the build time).
+constexpr int kRegK = 10;
+
+// The same factorisation for K <= kRegK, register-resident: lane i holds row i of
 // G; the right-looking update takes the pivot and the column entries from the
 // owning lanes by shuffle, and L^{-1} is formed column-per-lane by forward
 // substitution over shuffled entries of L. No shared-memory round trips, one
@@ -422,7 +427,7 @@ __device__ __noinline__ bool cholqr_pass_k(double* W, int64_t rows, double* smal
   gram_tall(W, rows, rows, K, G);
   if (threadIdx.x == 0) sc.ibcast[2] = 0;
   __syncthreads();
-  if constexpr (K <= 16)
+  if constexpr (K <= kRegK)
     chol_inv_warp_reg<K>(G, Li, sc, rel_pivot);
   else
     chol_inv_warp(G, K, L, Li, sc);
@@ -710,8 +715,8 @@ __device__ __noinline__ double* sym_topk_si_k(const double* __restrict__ G, int 
   const double* Gp = G;
   int ldp = n;
   // room for the register-tiled product's K-contiguous copy and partial sums
-  // (k <= 16: one out-of-line copy per K keeps the build time in check)
-  const bool tiled = K <= 16 && staged && n <= int(blockDim.x) &&
+  // (k <= kRegK: one out-of-line copy per K keeps the build time in check)
+  const bool tiled = K <= kRegK && staged && n <= int(blockDim.x) &&
                      topk_stage_off(K) + ldg * n + 3 * n * K + int(blockDim.x) * K <= sc.dsm_cap;
   double* const utr = dsm + topk_stage_off(K) + ldg * n + 2 * n * K;
   double* const part = utr + n * K;
@@ -734,7 +739,7 @@ __device__ __noinline__ double* sym_topk_si_k(const double* __restrict__ G, int 
   for (; it < kGramSiMaxIter; ++it) {
     long long tp = tstart();
     if (tiled) {
-      if constexpr (K <= 16) sym_gu_tiled<K>(Gp, ldp, n, U, W, utr, part);
+      if constexpr (K <= kRegK) sym_gu_tiled<K>(Gp, ldp, n, U, W, utr, part);
     } else {
       for (int idx = threadIdx.x; idx < n * K; idx += blockDim.x) {
         const int i = idx % n, j = idx / n;
@@ -798,7 +803,7 @@ __device__ __noinline__ double* sym_topk_si_k(const double* __restrict__ G, int 
       const long long tpw = tstart();
       for (int e = 0; e < extra; ++e) {  // U <- G W, then swap: W holds G^(1+e+1) U_old
         if (tiled) {
-          if constexpr (K <= 16) sym_gu_tiled<K>(Gp, ldp, n, W, U, utr, part);
+          if constexpr (K <= kRegK) sym_gu_tiled<K>(Gp, ldp, n, W, U, utr, part);
         } else {
           for (int idx = threadIdx.x; idx < n * K; idx += blockDim.x) {
             const int i = idx % n, j = idx / n;
@@ -881,7 +886,7 @@ __device__ __forceinline__ bool llsv_uses_subspace(int64_t rows, int64_t cols, i
   return si != nullptr && kprev > 0 && rows > cols && cols >= 2 * k && cols * k <= kSiMaxYK && k <= kSiMaxK &&
          si_base() + kSiMaxYK + 5 * k * k + 256 <= sc.dsm_cap;
 }
-// Two CholeskyQR passes on W (rows x k, ld rows), k <= 16; false on a breakdown
+// Two CholeskyQR passes on W (rows x k, ld rows), k <= kRegK; false on a breakdown
 // or when a column collapses against the earlier ones (CGS2's completion case;
 // W is then unchanged or still spans the same space). small: 3 k^2 doubles.
 static __device__ bool cholqr2(double* W, int64_t rows, int k, double* small, BlockScratch& sc) {
@@ -890,7 +895,7 @@ static __device__ bool cholqr2(double* W, int64_t rows, int k, double* small, Bl
   case N:          \
     return cholqr_pass_k<N>(W, rows, small, sc, 0.25) && cholqr_pass_k<N>(W, rows, small, sc);
     TT_CASE(1) TT_CASE(2) TT_CASE(3) TT_CASE(4) TT_CASE(5) TT_CASE(6) TT_CASE(7) TT_CASE(8)
-    TT_CASE(9) TT_CASE(10) TT_CASE(11) TT_CASE(12) TT_CASE(13) TT_CASE(14) TT_CASE(15) TT_CASE(16)
+    TT_CASE(9) TT_CASE(10)
 #undef TT_CASE
     default:
       return false;
@@ -1091,7 +1096,7 @@ static __device__ void llsv_unfold(const double* P, int64_t outer, int64_t rows,
     // Q as Gram-Schmidt (the QR factor with positive diagonal is unique) in two
     // short passes instead of ~4 block reductions per column; a rank-deficient U
     // (zeroed columns) breaks the Cholesky down and takes CGS2 with completion.
-    if (!(k <= 16 && 3 * k * k <= sc.dsm_cap && cholqr2(U, rows, int(k), dsm, sc)))
+    if (!(k <= kRegK && 3 * k * k <= sc.dsm_cap && cholqr2(U, rows, int(k), dsm, sc)))
       orthonormalize(U, rows, 0, int(k), rows, sc);
     tstop(sc, kPhOrtho, to);
   }

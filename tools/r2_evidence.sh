@@ -1,6 +1,6 @@
 # round-2 evidence pass: GPU suite, smoke, bench lines (default C3 stream, reference arm, burst configs),
 # ncu launch list of the bench + --set full captures of the streamed kernel, a solver kernel and the cluster stitch
-T=${TAG:-r2g}; O=gpurun_out/$T; mkdir -p $O
+T=${TAG:-r2i}; O=gpurun_out/$T; mkdir -p $O
 timeout 2700 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
 timeout 900 python bench.py > $O/bench_default.log 2>&1; echo "rc=$?" >> $O/bench_default.log
