@@ -1,22 +1,27 @@
-// Grid-wide leaf path — tucker_als (tucker.cpp:86-119) on a WIDE batch of
-// equal-length leaf blocks (the burst build of a tree), run as phase kernels
-// over all leaves instead of one CTA per leaf:
+// Grid-wide leaf path — tucker_als (tucker.cpp:86-119) on a batch of
+// equal-length leaf blocks (a tree build, a streamed leaf, a query's raw
+// tail), run as phase kernels over all leaves instead of one CTA per leaf:
 //
 //   per sweep   grid_ttm_kernel   Y_l = X_l x_1 U_1^T   every leaf, tiles across the whole GPU
+//               grid_last_kernel  Y x_2 U_2^T (order 3)  whole GPU
 //               grid_solve0       remaining small products, U_0 = llsv(M_0(Y))   one CTA per leaf
 //               grid_ttm_kernel   W_l = X_l x_0 U_0^T   every leaf, tiles across the whole GPU
 //   per mode    grid_ttm / grid_last   first (W-sized) product of the mode's chain, whole GPU
-//     n >= 1    grid_solve_mode   rest of the chain, U_n = llsv; last mode: core, fit / stop   one CTA per leaf
+//     n >= 1    grid_gram_kernel  partial Grams of the dense mode-1 unfolding (16 row chunks per leaf)
+//               grid_solve_mode   rest of the chain, U_n = llsv; last mode: core, fit / stop   one CTA per leaf
 //
-// Same arithmetic, mode order and stop rule as leaf_als_kernel (tt_leaf.cu);
-// only the two passes over X — >95% of a C3 leaf's bytes and flops — leave the
-// per-leaf CTA. grid_ttm_kernel is a persistent kernel (one CTA per SM): a
-// producer warp streams X tiles and the matching rows of the transposed,
-// zero-padded factor through a cp.async.bulk ring (full/empty mbarriers), and
-// 256 consumer threads each own TT consecutive columns of one slab and RC
-// accumulator columns in registers (RC*TT DFMAs per 1-2 LDS.128 of X and RC/2
-// broadcast LDS.128 of U^T). X is read from HBM once per pass and never staged
-// through a per-leaf workspace.
+// Same arithmetic, mode order and stop rule as leaf_als_kernel (tt_leaf.cu;
+// the streamed products accumulate in the same order, so the two paths agree
+// bit for bit on a build); the passes over X — >95% of a C3 leaf's bytes and
+// flops — and the W-sized products leave the per-leaf CTA. grid_ttm_kernel is
+// a persistent kernel (one CTA per SM): a producer warp streams X tiles and
+// the matching rows of the transposed, zero-padded factor through a 5-stage
+// cp.async.bulk ring (full/empty mbarriers), and 256 consumer threads each own
+// TT consecutive columns of one slab and RC accumulator columns in registers
+// (RC*TT DFMAs per 1-2 LDS.128 of X and RC/2 broadcast LDS.128 of U^T). X is
+// read from HBM once per pass (ncu: 4.34 GB for 4.33 GB of X at C3) and never
+// staged through a per-leaf workspace. Small batches take one slab and two
+// columns per thread so that a single leaf still spreads over the GPU.
 //
 // The per-leaf ALS state (column counts, ||X||^2, previous fit, stop flag)
 // lives in the leaf's workspace (GridWs::state); converged leaves are skipped
