@@ -20,9 +20,10 @@ slices under its range and the ALS seed (sst.cpp:83-92, 133-143), so:
   tensors and reassembled in query order. U_0 (L x r_0 per query, the bulk of
   the output) stays on the producing rank.
 
-The device work goes through a backend: `EngineBackend` (the CUDA engine's C
-ABI) or, in the CPU tests, `OracleBackend` (the restated reference) — the
-orchestration and the collectives are the same code.
+The device work goes through a backend object: `EngineBackend` (the CUDA
+engine's C ABI) is the only one in the package. The world-size-2 gloo tests
+pass a test double built on the CPU oracle (tests/oracle_backend.py) through
+the same orchestration and collectives.
 """
 from __future__ import annotations
 
@@ -201,60 +202,6 @@ class EngineBackend:
     def answer(self, tree, ranges):
         res = tree.range_query_batch([tuple(int(v) for v in r) for r in ranges]) if len(ranges) else []
         return [Payload(f.core, f.factors, f.objective, f.sweeps) for f in res]
-
-
-class OracleBackend:
-    """The same device-work interface on the CPU restatement (tests only)."""
-
-    def __init__(self, nontemporal, ranks, leaf_block, series, theta=0.7, max_iters=20, tol=0.01, seed=20240117):
-        self.nontemporal, self.ranks, self.B = tuple(nontemporal), tuple(ranks), leaf_block
-        self.theta, self.max_iters, self.tol, self.seed = theta, max_iters, tol, seed
-        self.series = series  # raw slices, for tail parts of queries
-
-    def subtree(self, x, n_slices, first_slice, on_device=False):
-        from oracle import oracle as O
-
-        t = O.Tree(self.nontemporal, self.ranks, theta=self.theta, max_iters=self.max_iters, tol=self.tol,
-                   seed=self.seed, leaf_block=self.B)
-        t.append(np.asarray(x)[:n_slices])
-        out = {}
-        for v in t.nodes():
-            if v.has_decomposition:
-                f = t.node_factors(v.id)
-                out[(v.begin + first_slice, v.end + first_slice)] = Payload(f.core, f.factors)
-        return out
-
-    def stitch(self, left, right):
-        from oracle import oracle as O
-
-        f = O.stitch([O.Factors(left.core, left.factors), O.Factors(right.core, right.factors)], self.ranks,
-                     self.max_iters, self.tol, self.seed)
-        return Payload(f.core, f.factors, f.objective, len(f.objective))
-
-    def assemble(self, gs, payloads):
-        return (gs, payloads)
-
-    def answer(self, tree, ranges):
-        """range_query_detailed (query.cpp:49-69) over gathered payloads: recall,
-        entire = stored, partial = partial_hit_factors, tail = tucker_als of the
-        raw tail, then stitch."""
-        from oracle import oracle as O
-
-        gs, payloads = tree
-        out = []
-        for ts, te in ranges:
-            parts = []
-            for h in gs.tree.recall(int(ts), int(te)):
-                if h.flag == 2:
-                    parts.append(O.tucker_als(self.series[h.begin:h.end], self.ranks, self.max_iters, self.tol,
-                                              self.seed))
-                    continue
-                v = gs.nodes[h.node - 1]
-                f = O.Factors(payloads[h.node].core, payloads[h.node].factors)
-                parts.append(f if h.flag == 0 else O.partial_hit_factors(f, h.begin - v.begin, h.end - v.begin))
-            f = O.stitch(parts, self.ranks, self.max_iters, self.tol, self.seed)
-            out.append(Payload(f.core, f.factors, f.objective, len(f.objective)))
-        return out
 
 
 # ---------------------------------------------------------------------------

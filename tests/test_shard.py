@@ -114,6 +114,7 @@ def _dist_worker(rank, world, port, out_q):
 
     from oracle import oracle as O
     from paper_2501_06647_b200 import distributed as D
+    from tests.oracle_backend import OracleBackend
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -124,7 +125,7 @@ def _dist_worker(rank, world, port, out_q):
         x = O.generate_synthetic([T, 5, 4], [3, 3, 2], 0.1, 9)
         plan = shard.plan_build(T // B, world)
         lo, hi = D.run_of(plan[rank], B)
-        be = D.OracleBackend(nt, ranks, B, x)
+        be = OracleBackend(nt, ranks, B, x)
         tree, gs, stats = D.build_sharded(be, x[lo:hi], T, plan, rank, "cpu")
         ranges = []
         while len(ranges) < 20:
